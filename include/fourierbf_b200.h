@@ -1,0 +1,125 @@
+/*
+ * fourierbf_b200.h -- the C-ABI boundary of the B200 shiftable bilateral filter.
+ *
+ * Plain C: pointers, sizes and status codes, no C++ or torch types.  These
+ * entry points replace the reference's hot path
+ *   fourierbf::bilateral_fast   /root/reference/proj/include/fourierbf/bilateral.hpp:109-160
+ *   fourierbf::convolve         /root/reference/proj/include/fourierbf/spatial.hpp:98-112
+ * The reference's own C++ API (the headers under include/fourierbf/) is
+ * implemented on top of them; INTEGRATION.md shows the ctypes binding.
+ *
+ * Errors follow the reference's conventions (bilateral.hpp:112-118,147-158):
+ *   FBF_EINVAL   <-> std::invalid_argument (empty image; eps >= w0; bad sizes)
+ *   FBF_EANOMALY <-> std::runtime_error "denominator collapsed at pixel (x, y)",
+ *                    *bad_index = first offending row-major index
+ * fbf_last_error() returns the thread's message for the last failing call.
+ * All entry points are reentrant: no global mutable state besides a cached
+ * per-device attribute table and the thread-local error string.
+ */
+#ifndef FOURIERBF_B200_H
+#define FOURIERBF_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FBF_OK 0
+#define FBF_EINVAL 1
+#define FBF_EANOMALY 2
+#define FBF_ECUDA 3
+#define FBF_EUNSUPPORTED 4
+
+#define FBF_SPATIAL_GAUSSIAN 0 /* spatial.hpp:13 SpatialKind::gaussian */
+#define FBF_SPATIAL_BOX 1      /* spatial.hpp:13 SpatialKind::box      */
+
+#define FBF_RANGE_GAUSSIAN 0    /* kernels.hpp:12 RangeFamily::gaussian    */
+#define FBF_RANGE_EXPONENTIAL 1 /* kernels.hpp:12 RangeFamily::exponential */
+
+#define FBF_VARIANT_FUSED 0 /* one fused kernel (default)                        */
+#define FBF_VARIANT_NAIVE 1 /* multi-kernel, HBM-resident planes (comparison)    */
+
+/* Where the pixels are.  The global image is width x height.  A buffer holds
+ * rows [src_row0, src_row0 + src_rows) of each of `batch` images (row strips
+ * for multi-GPU sharding carry their W halo rows); rows [out_row0, out_row0 +
+ * out_rows) are produced.  Pitches / strides are in elements. */
+typedef struct fbf_geometry {
+  int width, height;
+  int batch;
+  int src_row0, src_rows;
+  int out_row0, out_rows;
+  long long src_pitch, dst_pitch;
+  long long src_bstride, dst_bstride;
+} fbf_geometry;
+
+/* SpatialKernel (spatial.hpp:22-33) + FourierKernelApprox (kernel_approx.hpp:19-44). */
+typedef struct fbf_filter {
+  int kind;               /* FBF_SPATIAL_*                                  */
+  int radius;             /* W                                              */
+  const double* profile;  /* 2W+1 normalised taps (host memory)             */
+  double w0;              /* centre weight profile[W]^2                     */
+  int N;                  /* highest harmonic                               */
+  const double* d;        /* d_0..d_N (host memory)                         */
+  double omega;           /* pi / T                                         */
+  double max_pointwise_error; /* epsilon of the fit                         */
+  int check_epsilon;      /* 1: enforce eps < w0 like bilateral.hpp:114-118 */
+} fbf_filter;
+
+const char* fbf_last_error(void);
+int fbf_version(void);
+
+/* Fills g for a whole single image (or a batch of contiguous images). */
+void fbf_geometry_whole(fbf_geometry* g, int width, int height, int batch);
+
+/* Device workspace needed by fbf_bilateral_fast_device (bytes). */
+size_t fbf_workspace_bytes(const fbf_geometry* g, int variant);
+
+/* Asynchronous, device-resident: src/dst/workspace are device pointers,
+ * `stream` a cudaStream_t (NULL = legacy default).  d_bad (device, may be
+ * NULL) receives atomicMin of the first collapsed-denominator linear index
+ * (b*H*W + y*W + x); the caller initialises it to ~0ULL. */
+int fbf_bilateral_fast_device(const fbf_geometry* g, const fbf_filter* f, const float* src,
+                              float* dst, void* workspace, size_t workspace_bytes,
+                              unsigned long long* d_bad, int variant, void* stream);
+
+/* Synchronous, host buffers (fp32): H2D, filter, D2H.  On FBF_EANOMALY
+ * *bad_index holds the first offending index. */
+int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const float* src,
+                            float* dst, int variant, long long* bad_index);
+
+/* Same on fp64 host buffers (the reference Image stores doubles). */
+int fbf_bilateral_fast_host_f64(const fbf_geometry* g, const fbf_filter* f, const double* src,
+                                double* dst, int variant, long long* bad_index);
+
+/* convolve (spatial.hpp:98-112), direct backend, fp32 on the device. */
+int fbf_convolve_device(int width, int height, const double* profile, int radius,
+                        const float* src, float* dst, void* workspace, size_t workspace_bytes,
+                        void* stream);
+int fbf_convolve_host_f64(int width, int height, const double* profile, int radius,
+                          const double* src, double* dst);
+
+/* Host-side pieces of the path (stay on the CPU, as in the reference). */
+int fbf_spatial_gaussian(double sigma_s, double* profile, int* radius, double* w0);
+int fbf_spatial_box(int radius, double* profile, double* w0);
+double fbf_range_eval(int family, double sigma_r, double t);
+int fbf_fit_fixed(int family, double sigma_r, int T, int N, double* d, double* residual_norm,
+                  double* max_pointwise_error);
+int fbf_progressive_fit(int family, double sigma_r, int T, double epsilon, double* d, int* N,
+                        double* residual_norm, double* max_pointwise_error);
+double fbf_error_bound(int T, double epsilon, double w0);
+
+/* Seeded synthetic image generator for the BASELINE configs (DESIGN.md
+ * "inputs"): rows [row0, row0+rows) of a width x height image into out
+ * (row-major, fp32), using nthreads host threads. */
+int fbf_synth_image(unsigned long long seed, int width, int height, int rects, double noise_sigma,
+                    int row0, int rows, float* out, int nthreads);
+
+/* FP32 FMA-pipe peak of the current device, measured by a resident FFMA2
+ * probe kernel: lane-ops per second and the SM clock it ran at. */
+int fbf_probe_fma_peak(double* ops_per_s, double* sm_mhz, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

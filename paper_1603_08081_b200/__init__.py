@@ -1,0 +1,293 @@
+"""paper_1603_08081_b200 -- B200-native shiftable Fourier-kernel bilateral filter.
+
+Python mirror of the reference's operator interface for the hot path
+(/root/reference/proj/include/fourierbf: ``make_spatial_gaussian``,
+``make_spatial_box``, ``progressive_fit``, ``bilateral_fast``, ``convolve``,
+``error_bound``), implemented as a thin ctypes layer over the C-ABI
+``include/fourierbf_b200.h`` of ``_lib/libfourierbf_b200.so``.  The native
+library is required: importing this package without it raises ImportError, and
+no call ever falls back to a CPU implementation.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libfourierbf_b200.so")
+
+FBF_OK, FBF_EINVAL, FBF_EANOMALY, FBF_ECUDA, FBF_EUNSUPPORTED = 0, 1, 2, 3, 4
+SPATIAL_GAUSSIAN, SPATIAL_BOX = 0, 1
+RANGE_GAUSSIAN, RANGE_EXPONENTIAL = 0, 1
+VARIANT_FUSED, VARIANT_NAIVE = 0, 1
+_VARIANTS = {"fused": VARIANT_FUSED, "naive": VARIANT_NAIVE}
+
+
+class Geometry(ctypes.Structure):
+    _fields_ = [
+        ("width", ctypes.c_int), ("height", ctypes.c_int), ("batch", ctypes.c_int),
+        ("src_row0", ctypes.c_int), ("src_rows", ctypes.c_int),
+        ("out_row0", ctypes.c_int), ("out_rows", ctypes.c_int),
+        ("src_pitch", ctypes.c_longlong), ("dst_pitch", ctypes.c_longlong),
+        ("src_bstride", ctypes.c_longlong), ("dst_bstride", ctypes.c_longlong),
+    ]
+
+
+class Filter(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int), ("radius", ctypes.c_int),
+        ("profile", ctypes.POINTER(ctypes.c_double)), ("w0", ctypes.c_double),
+        ("N", ctypes.c_int), ("d", ctypes.POINTER(ctypes.c_double)),
+        ("omega", ctypes.c_double), ("max_pointwise_error", ctypes.c_double),
+        ("check_epsilon", ctypes.c_int),
+    ]
+
+
+# name -> (restype, argtypes): every symbol include/fourierbf_b200.h declares
+_P = ctypes.c_void_p
+_D = ctypes.POINTER(ctypes.c_double)
+_F = ctypes.POINTER(ctypes.c_float)
+_I = ctypes.POINTER(ctypes.c_int)
+_LL = ctypes.POINTER(ctypes.c_longlong)
+SIGNATURES = {
+    "fbf_last_error": (ctypes.c_char_p, []),
+    "fbf_version": (ctypes.c_int, []),
+    "fbf_geometry_whole": (None, [ctypes.POINTER(Geometry), ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "fbf_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(Geometry), ctypes.c_int]),
+    "fbf_bilateral_fast_device": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.POINTER(Filter), _P, _P, _P,
+                                                 ctypes.c_size_t, _P, ctypes.c_int, _P]),
+    "fbf_bilateral_fast_host": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.POINTER(Filter), _F, _F,
+                                               ctypes.c_int, _LL]),
+    "fbf_bilateral_fast_host_f64": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.POINTER(Filter), _D, _D,
+                                                   ctypes.c_int, _LL]),
+    "fbf_convolve_device": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _D, ctypes.c_int, _P, _P, _P,
+                                           ctypes.c_size_t, _P]),
+    "fbf_convolve_host_f64": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _D, ctypes.c_int, _D, _D]),
+    "fbf_spatial_gaussian": (ctypes.c_int, [ctypes.c_double, _D, _I, _D]),
+    "fbf_spatial_box": (ctypes.c_int, [ctypes.c_int, _D, _D]),
+    "fbf_range_eval": (ctypes.c_double, [ctypes.c_int, ctypes.c_double, ctypes.c_double]),
+    "fbf_fit_fixed": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int, _D, _D, _D]),
+    "fbf_progressive_fit": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_double, _D,
+                                           _I, _D, _D]),
+    "fbf_error_bound": (ctypes.c_double, [ctypes.c_int, ctypes.c_double, ctypes.c_double]),
+    "fbf_synth_image": (ctypes.c_int, [ctypes.c_ulonglong, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_double, ctypes.c_int, ctypes.c_int, _F, ctypes.c_int]),
+    "fbf_probe_fma_peak": (ctypes.c_int, [_D, _D, _P]),
+}
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback for the filter)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+class FilterError(RuntimeError):
+    """std::runtime_error of the reference (numerical anomaly, CUDA failure)."""
+
+
+def _check(rc: int) -> None:
+    if rc == FBF_OK:
+        return
+    msg = lib.fbf_last_error().decode()
+    if rc == FBF_EINVAL:
+        raise ValueError(msg)  # std::invalid_argument
+    raise FilterError(msg)
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(_D)
+
+
+# --------------------------------------------------------------------- types
+
+@dataclass
+class SpatialKernel:
+    """spatial.hpp:22-33"""
+    kind: int
+    sigma_s: float
+    radius: int
+    profile: np.ndarray
+    w0: float
+
+    def weight(self, dx: int, dy: int) -> float:
+        return float(self.profile[dx + self.radius] * self.profile[dy + self.radius])
+
+
+@dataclass
+class FourierKernelApprox:
+    """kernel_approx.hpp:19-44"""
+    T: int
+    omega: float
+    N: int
+    d: np.ndarray
+    residual_norm: float = 0.0
+    max_pointwise_error: float = 0.0
+
+    def evaluate(self, t):
+        n = np.arange(self.N + 1)
+        return np.cos(np.multiply.outer(np.asarray(t, dtype=np.float64), n * self.omega)) @ self.d
+
+
+def make_spatial_gaussian(sigma_s: float) -> SpatialKernel:
+    r = ctypes.c_int()
+    if lib.fbf_spatial_gaussian(float(sigma_s), None, ctypes.byref(r), None) != FBF_OK:
+        raise ValueError("spatial sigma must be positive")
+    prof = np.zeros(2 * r.value + 1)
+    w0 = ctypes.c_double()
+    lib.fbf_spatial_gaussian(float(sigma_s), _dp(prof), ctypes.byref(r), ctypes.byref(w0))
+    return SpatialKernel(SPATIAL_GAUSSIAN, float(sigma_s), r.value, prof, w0.value)
+
+
+def make_spatial_box(radius: int) -> SpatialKernel:
+    if radius < 1:
+        raise ValueError("box radius must be at least 1")
+    prof = np.zeros(2 * radius + 1)
+    w0 = ctypes.c_double()
+    lib.fbf_spatial_box(int(radius), _dp(prof), ctypes.byref(w0))
+    return SpatialKernel(SPATIAL_BOX, 0.0, int(radius), prof, w0.value)
+
+
+def fit_fixed(family: int, sigma_r: float, T: int, N: int) -> FourierKernelApprox:
+    """Fixed-order least-squares fit via the recursive QR (acceptance.cpp:247-263 pattern)."""
+    d = np.zeros(N + 1)
+    rn, mx = ctypes.c_double(), ctypes.c_double()
+    _check(lib.fbf_fit_fixed(family, float(sigma_r), int(T), int(N), _dp(d), ctypes.byref(rn), ctypes.byref(mx)))
+    return FourierKernelApprox(int(T), float(np.pi / T), int(N), d, rn.value, mx.value)
+
+
+def progressive_fit(family: int, sigma_r: float, T: int, epsilon: float) -> FourierKernelApprox:
+    """kernel_approx.hpp:169-219"""
+    d = np.zeros(T + 1)
+    n = ctypes.c_int()
+    rn, mx = ctypes.c_double(), ctypes.c_double()
+    _check(lib.fbf_progressive_fit(family, float(sigma_r), int(T), float(epsilon), _dp(d), ctypes.byref(n),
+                                   ctypes.byref(rn), ctypes.byref(mx)))
+    return FourierKernelApprox(int(T), float(np.pi / T), n.value, d[: n.value + 1].copy(), rn.value, mx.value)
+
+
+def error_bound(T: int, epsilon: float, w0: float) -> float:
+    """analysis.hpp:27-34"""
+    if T < 0 or not epsilon >= 0.0 or not epsilon < w0:
+        raise ValueError("error_bound: tolerance must stay below the center spatial weight")
+    return lib.fbf_error_bound(int(T), float(epsilon), float(w0))
+
+
+def _filter_struct(spatial: SpatialKernel, approx: FourierKernelApprox, check_epsilon: bool = True):
+    prof = np.ascontiguousarray(spatial.profile, dtype=np.float64)
+    d = np.ascontiguousarray(approx.d, dtype=np.float64)
+    f = Filter(spatial.kind, spatial.radius, _dp(prof), spatial.w0, approx.N, _dp(d), approx.omega,
+               approx.max_pointwise_error, 1 if check_epsilon else 0)
+    f._keep = (prof, d)  # keep the buffers alive with the struct
+    return f
+
+
+def whole_geometry(width: int, height: int, batch: int = 1) -> Geometry:
+    g = Geometry()
+    lib.fbf_geometry_whole(ctypes.byref(g), int(width), int(height), int(batch))
+    return g
+
+
+def strip_geometry(width: int, height: int, out_row0: int, out_rows: int, radius: int,
+                   batch: int = 1) -> Geometry:
+    """Row strip [out_row0, out_row0+out_rows) with its W halo rows (mirror only at global edges)."""
+    lo = max(0, out_row0 - radius)
+    hi = min(height, out_row0 + out_rows + radius)
+    if height <= 2 * radius + 1:
+        lo, hi = 0, height
+    g = Geometry()
+    g.width, g.height, g.batch = width, height, batch
+    g.src_row0, g.src_rows = lo, hi - lo
+    g.out_row0, g.out_rows = out_row0, out_rows
+    g.src_pitch = g.dst_pitch = width
+    g.src_bstride = (hi - lo) * width
+    g.dst_bstride = out_rows * width
+    return g
+
+
+def bilateral_fast(image: np.ndarray, spatial: SpatialKernel, approx: FourierKernelApprox,
+                   variant: str = "fused", check_epsilon: bool = True) -> np.ndarray:
+    """bilateral.hpp:109-160 on the GPU: host array in, host array out (fp32 compute).
+
+    ``image`` is (H, W) or (B, H, W); float64 or float32.  Raises ValueError
+    (invalid_argument) / FilterError (runtime_error) like the reference.
+    """
+    a = np.asarray(image)
+    if a.size == 0:
+        raise ValueError("bilateral_fast: empty image")
+    batch = 1 if a.ndim == 2 else a.shape[0]
+    h, w = a.shape[-2], a.shape[-1]
+    g = whole_geometry(w, h, batch)
+    f = _filter_struct(spatial, approx, check_epsilon)
+    bad = ctypes.c_longlong(-1)
+    if a.dtype == np.float32:
+        src = np.ascontiguousarray(a)
+        out = np.empty_like(src)
+        rc = lib.fbf_bilateral_fast_host(ctypes.byref(g), ctypes.byref(f), src.ctypes.data_as(_F),
+                                         out.ctypes.data_as(_F), _VARIANTS[variant], ctypes.byref(bad))
+    else:
+        src = np.ascontiguousarray(a, dtype=np.float64)
+        out = np.empty_like(src)
+        rc = lib.fbf_bilateral_fast_host_f64(ctypes.byref(g), ctypes.byref(f), _dp(src), _dp(out),
+                                             _VARIANTS[variant], ctypes.byref(bad))
+    _check(rc)
+    return out
+
+
+def bilateral_fast_device(src_ptr: int, dst_ptr: int, geometry: Geometry, spatial: SpatialKernel,
+                          approx: FourierKernelApprox, workspace_ptr: int, workspace_bytes: int,
+                          bad_ptr: int, stream: int = 0, variant: str = "fused",
+                          check_epsilon: bool = True) -> None:
+    """Asynchronous device-resident call (pointers from torch tensors, cudaStream_t as int)."""
+    f = _filter_struct(spatial, approx, check_epsilon)
+    _check(lib.fbf_bilateral_fast_device(ctypes.byref(geometry), ctypes.byref(f), src_ptr, dst_ptr,
+                                         workspace_ptr, workspace_bytes, bad_ptr, _VARIANTS[variant], stream))
+
+
+def workspace_bytes(geometry: Geometry, variant: str = "fused") -> int:
+    return int(lib.fbf_workspace_bytes(ctypes.byref(geometry), _VARIANTS[variant]))
+
+
+def convolve(plane: np.ndarray, spatial: SpatialKernel) -> np.ndarray:
+    """spatial.hpp:98-112 (direct backend) on the GPU."""
+    p = np.ascontiguousarray(plane, dtype=np.float64)
+    if p.size == 0:
+        raise ValueError("convolve: empty plane")
+    out = np.empty_like(p)
+    prof = np.ascontiguousarray(spatial.profile, dtype=np.float64)
+    _check(lib.fbf_convolve_host_f64(p.shape[1], p.shape[0], _dp(prof), spatial.radius, _dp(p), _dp(out)))
+    return out
+
+
+def synth_image(seed: int, width: int, height: int, rects: int, noise_sigma: float,
+                row0: int = 0, rows: Optional[int] = None, nthreads: int = 0) -> np.ndarray:
+    """BASELINE.json's seeded synthetic image, rows [row0, row0+rows)."""
+    rows = height - row0 if rows is None else rows
+    out = np.empty((rows, width), dtype=np.float32)
+    nt = nthreads or min(32, os.cpu_count() or 1)
+    _check(lib.fbf_synth_image(int(seed), int(width), int(height), int(rects), float(noise_sigma),
+                               int(row0), int(rows), out.ctypes.data_as(_F), nt))
+    return out
+
+
+def probe_fma_peak(stream: int = 0):
+    ops, mhz = ctypes.c_double(), ctypes.c_double()
+    _check(lib.fbf_probe_fma_peak(ctypes.byref(ops), ctypes.byref(mhz), stream))
+    return ops.value, mhz.value
+
+
+from . import configs  # noqa: E402,F401

@@ -1,0 +1,633 @@
+// fbf_capi.cu -- the extern "C" boundary (include/fourierbf_b200.h) plus the
+// small kernels around the fused one: the phase prep, the naive multi-kernel
+// variant (HBM-resident planes), the standalone separable convolution and the
+// FP32 FMA-pipe peak probe used as the roofline denominator.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "fbf_device.cuh"
+#include "fbf_params.h"
+#include "fourierbf_b200.h"
+
+namespace fbf {
+bool fused_supported(int W);
+cudaError_t launch_fused(const FusedArgs& a, cudaStream_t st, int* grid_out);
+}  // namespace fbf
+
+using namespace fbf;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(FBF_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define FBF_CUDA(call)                                  \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+size_t align256(size_t n) { return (n + 255) & ~size_t(255); }
+
+// ---------------------------------------------------------------------------
+// prep: (u, f') per source pixel.  u = round(f' * omega/(2 pi) * 2^32) mod 2^32
+// in fp64 (exact base phase in turns), f' = f - shift.
+
+__global__ void prep_kernel(const float* __restrict__ src, int2* __restrict__ uf, Geometry g,
+                            double turns_scaled, float shift) {
+  const long long per = static_cast<long long>(g.src_rows) * g.width;
+  const long long total = per * g.batch;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long b = i / per;
+    const long long r = i - b * per;
+    const int y = static_cast<int>(r / g.width);
+    const int x = static_cast<int>(r - static_cast<long long>(y) * g.width);
+    const float f = src[b * g.src_bstride + static_cast<long long>(y) * g.src_pitch + x];
+    const double fd = static_cast<double>(f) - static_cast<double>(shift);
+    const long long u = __double2ll_rn(fd * turns_scaled);
+    uf[i] = make_int2(static_cast<int>(static_cast<unsigned>(u)),
+                                                  __float_as_int(static_cast<float>(fd)));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// naive variant: per harmonic four kernels over HBM-resident float4 planes
+//   modulate -> row FIR -> column FIR -> demodulate, then one divide kernel.
+
+struct NaiveArgs {
+  Geometry g;  // uf / planes use a dense layout: batch x src_rows x width
+  Taps k;
+};
+
+__global__ void naive_modulate(const int2* __restrict__ uf, float4* __restrict__ M, long long total,
+                               uint32_t n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int2 v = uf[i];
+    float c, s;
+    sincos_turns(n * static_cast<uint32_t>(v.x), c, s);
+    const float fp = __int_as_float(v.y);
+    M[i] = make_float4(c, c * fp, s, s * fp);
+  }
+}
+
+__global__ void naive_rows(const float4* __restrict__ in, float4* __restrict__ out,
+                           const __grid_constant__ NaiveArgs a) {
+  const long long per = static_cast<long long>(a.g.src_rows) * a.g.width;
+  const long long total = per * a.g.batch;
+  const int W = a.k.W;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long rowbase = i - (i % a.g.width);
+    const int x = static_cast<int>(i % a.g.width);
+    f2 A{0.f, 0.f}, B{0.f, 0.f};
+    for (int j = -W; j <= W; ++j) {  // out(x) = sum_j p[j] in(x - j), spatial.hpp:82-86
+      const float4 v = in[rowbase + mirror_index(x - j, a.g.width)];
+      const int tj = j < 0 ? -j : j;
+      const float tv = a.k.t[tj];
+      const f2 t{tv, tv};
+      ffma2(A, t, f2{v.x, v.y});
+      ffma2(B, t, f2{v.z, v.w});
+    }
+    out[i] = make_float4(A.x, A.y, B.x, B.y);
+  }
+}
+
+__global__ void naive_cols(const float4* __restrict__ in, float4* __restrict__ out,
+                           const __grid_constant__ NaiveArgs a) {
+  const long long per_out = static_cast<long long>(a.g.out_rows) * a.g.width;
+  const long long per_src = static_cast<long long>(a.g.src_rows) * a.g.width;
+  const long long total = per_out * a.g.batch;
+  const int W = a.k.W;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long b = i / per_out;
+    const long long r = i - b * per_out;
+    const int y = a.g.out_row0 + static_cast<int>(r / a.g.width);
+    const int x = static_cast<int>(r % a.g.width);
+    const float4* src = in + b * per_src;
+    f2 A{0.f, 0.f}, B{0.f, 0.f};
+    for (int j = -W; j <= W; ++j) {
+      const int sy = mirror_index(y - j, a.g.full_height) - a.g.src_row0;
+      const float4 v = src[static_cast<long long>(sy) * a.g.width + x];
+      const int tj = j < 0 ? -j : j;
+      const float tv = a.k.t[tj];
+      const f2 t{tv, tv};
+      ffma2(A, t, f2{v.x, v.y});
+      ffma2(B, t, f2{v.z, v.w});
+    }
+    out[i] = make_float4(A.x, A.y, B.x, B.y);
+  }
+}
+
+__global__ void naive_demod(const float4* __restrict__ M, const float4* __restrict__ C,
+                            Pair* __restrict__ pq, Geometry g, float dn, int first) {
+  const long long per_out = static_cast<long long>(g.out_rows) * g.width;
+  const long long per_src = static_cast<long long>(g.src_rows) * g.width;
+  const long long total = per_out * g.batch;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long b = i / per_out;
+    const long long r = i - b * per_out;
+    const int y = g.out_row0 + static_cast<int>(r / g.width);
+    const int x = static_cast<int>(r % g.width);
+    const float4 m = M[b * per_src + static_cast<long long>(y - g.src_row0) * g.width + x];
+    const float4 c = C[i];
+    f2 qp = mul2(f2{m.x, m.x}, f2{c.x, c.y});
+    qp = fma2(f2{m.z, m.z}, f2{c.z, c.w}, qp);
+    f2 acc = first ? mul2(f2{dn, dn}, qp) : fma2(f2{dn, dn}, qp, f2{pq[i].x, pq[i].y});
+    pq[i] = Pair{acc.x, acc.y};
+  }
+}
+
+__global__ void finish_kernel(const Pair* __restrict__ pq, float* __restrict__ dst, Geometry g,
+                              float shift, float q_floor, unsigned long long* bad) {
+  const long long per_out = static_cast<long long>(g.out_rows) * g.width;
+  const long long total = per_out * g.batch;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long b = i / per_out;
+    const long long r = i - b * per_out;
+    const int yl = static_cast<int>(r / g.width);
+    const int x = static_cast<int>(r % g.width);
+    const Pair v = pq[i];
+    if (!(fabsf(v.x) >= q_floor) && bad) {
+      const unsigned long long lin = static_cast<unsigned long long>(b) * g.full_height * g.width +
+                                     static_cast<unsigned long long>(g.out_row0 + yl) * g.width + x;
+      atomicMin(bad, lin);
+    }
+    dst[b * g.dst_bstride + static_cast<long long>(yl) * g.dst_pitch + x] = shift + __fdiv_rn(v.y, v.x);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// standalone separable convolution of one fp32 plane (convolve(), spatial.hpp:98-112)
+
+__global__ void conv_rows_f32(const float* __restrict__ in, float* __restrict__ out, int w, int h,
+                              const __grid_constant__ Taps k) {
+  const long long total = static_cast<long long>(w) * h;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long rowbase = i - (i % w);
+    const int x = static_cast<int>(i % w);
+    float acc = 0.f;
+    for (int j = -k.W; j <= k.W; ++j) acc = fmaf(k.t[j < 0 ? -j : j], in[rowbase + mirror_index(x - j, w)], acc);
+    out[i] = acc;
+  }
+}
+
+__global__ void conv_cols_f32(const float* __restrict__ in, float* __restrict__ out, int w, int h,
+                              const __grid_constant__ Taps k) {
+  const long long total = static_cast<long long>(w) * h;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int y = static_cast<int>(i / w);
+    const int x = static_cast<int>(i % w);
+    float acc = 0.f;
+    for (int j = -k.W; j <= k.W; ++j)
+      acc = fmaf(k.t[j < 0 ? -j : j], in[static_cast<long long>(mirror_index(y - j, h)) * w + x], acc);
+    out[i] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FP32 FMA-pipe probe: 16 independent FFMA2 chains per thread.
+
+__global__ void __launch_bounds__(256) fma_probe(float* out, float a, float b, int iters,
+                                                 long long* cycles) {
+  f2 acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = f2{threadIdx.x * 1e-3f + i, static_cast<float>(i)};
+  const f2 ma{a, a}, mb{b, b};
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = fma2(acc[i], ma, mb);
+  }
+  const long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += acc[i].x + acc[i].y;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+}
+
+unsigned grid_for(long long n, int threads) {
+  long long g = (n + threads - 1) / threads;
+  g = std::min<long long>(g, 148LL * 32);
+  return static_cast<unsigned>(std::max<long long>(g, 1));
+}
+
+int check_geometry(const fbf_geometry* g) {
+  if (!g) return fail(FBF_EINVAL, "bilateral_fast: null geometry");
+  if (g->width <= 0 || g->height <= 0 || g->batch <= 0)
+    return fail(FBF_EINVAL, "bilateral_fast: empty image");
+  if (g->src_row0 < 0 || g->src_rows <= 0 || g->src_row0 + g->src_rows > g->height ||
+      g->out_row0 < 0 || g->out_rows <= 0 || g->out_row0 + g->out_rows > g->height)
+    return fail(FBF_EINVAL, "bilateral_fast: row range outside the image");
+  return FBF_OK;
+}
+
+int check_filter(const fbf_filter* f) {
+  if (!f || !f->profile || !f->d) return fail(FBF_EINVAL, "bilateral_fast: null filter");
+  if (f->radius < 1 || f->radius > kMaxW)
+    return fail(FBF_EUNSUPPORTED, "bilateral_fast: spatial radius outside [1, 64]");
+  if (f->N < 0 || f->N > kMaxN)
+    return fail(FBF_EUNSUPPORTED, "bilateral_fast: harmonic count outside [0, 127]");
+  if (f->check_epsilon && !(f->max_pointwise_error < f->w0))
+    return fail(FBF_EINVAL,
+                "bilateral_fast: kernel approximation error must stay below the center "
+                "spatial weight");
+  return FBF_OK;
+}
+
+// The source rows must cover every mirrored row that the output rows touch.
+int check_halo(const fbf_geometry* g, int W) {
+  int lo = g->height, hi = -1;
+  auto visit = [&](int y) {
+    for (int k = -W; k <= W; ++k) {
+      const int s = mirror_index(y + k, g->height);
+      lo = std::min(lo, s);
+      hi = std::max(hi, s);
+    }
+  };
+  const int a = g->out_row0, b = g->out_row0 + g->out_rows;
+  for (int y = a; y < std::min(b, a + 2 * W + 1); ++y) visit(y);
+  for (int y = std::max(a, b - 2 * W - 1); y < b; ++y) visit(y);
+  if (lo < g->src_row0 || hi >= g->src_row0 + g->src_rows)
+    return fail(FBF_EINVAL, "bilateral_fast: source strip lacks the W halo rows the output needs");
+  return FBF_OK;
+}
+
+Geometry to_geometry(const fbf_geometry* g) {
+  Geometry G{};
+  G.width = g->width;
+  G.full_height = g->height;
+  G.src_row0 = g->src_row0;
+  G.src_rows = g->src_rows;
+  G.out_row0 = g->out_row0;
+  G.out_rows = g->out_rows;
+  G.batch = g->batch;
+  G.src_bstride = g->src_bstride;
+  G.src_pitch = static_cast<int>(g->src_pitch);
+  G.dst_bstride = g->dst_bstride;
+  G.dst_pitch = static_cast<int>(g->dst_pitch);
+  return G;
+}
+
+void fill_taps(Taps& k, const fbf_filter* f) {
+  std::memset(&k, 0, sizeof(k));
+  k.W = f->radius;
+  k.box = f->kind == FBF_SPATIAL_BOX;
+  k.box_tap = static_cast<float>(f->profile[f->radius]);
+  for (int j = 0; j <= f->radius; ++j) {
+    k.t[j] = static_cast<float>(f->profile[f->radius + j]);
+  }
+}
+
+void fill_harmonics(Harmonics& h, const fbf_filter* f) {
+  std::memset(&h, 0, sizeof(h));
+  h.N = f->N;
+  for (int n = 0; n <= f->N; ++n) h.d[n] = static_cast<float>(f->d[n]);
+  h.turns_per_unit = f->omega / (2.0 * M_PI);
+  h.shift = 128.0f;
+  h.q_floor = static_cast<float>((f->w0 - f->max_pointwise_error) / 2.0);
+}
+
+struct Layout {
+  size_t uf, pq, m, t, c, total;
+};
+
+Layout layout_of(const fbf_geometry* g, int variant) {
+  Layout L{};
+  const size_t src_px = static_cast<size_t>(g->batch) * g->src_rows * g->width;
+  const size_t out_px = static_cast<size_t>(g->batch) * g->out_rows * g->width;
+  L.uf = 0;
+  L.pq = align256(src_px * sizeof(int2));
+  size_t end = L.pq + align256(out_px * sizeof(Pair));
+  if (variant == FBF_VARIANT_NAIVE) {
+    L.m = end;
+    L.t = L.m + align256(src_px * sizeof(float4));
+    L.c = L.t + align256(src_px * sizeof(float4));
+    end = L.c + align256(out_px * sizeof(float4));
+  }
+  L.total = end;
+  return L;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fbf_last_error(void) { return g_err.c_str(); }
+int fbf_version(void) { return 1; }
+
+void fbf_geometry_whole(fbf_geometry* g, int width, int height, int batch) {
+  g->width = width;
+  g->height = height;
+  g->batch = batch;
+  g->src_row0 = 0;
+  g->src_rows = height;
+  g->out_row0 = 0;
+  g->out_rows = height;
+  g->src_pitch = width;
+  g->dst_pitch = width;
+  g->src_bstride = static_cast<long long>(width) * height;
+  g->dst_bstride = static_cast<long long>(width) * height;
+}
+
+size_t fbf_workspace_bytes(const fbf_geometry* g, int variant) {
+  if (check_geometry(g) != FBF_OK) return 0;
+  return layout_of(g, variant).total;
+}
+
+int fbf_bilateral_fast_device(const fbf_geometry* gp, const fbf_filter* f, const float* src,
+                              float* dst, void* workspace, size_t workspace_bytes,
+                              unsigned long long* d_bad, int variant, void* stream) {
+  int rc = check_geometry(gp);
+  if (rc) return rc;
+  if ((rc = check_filter(f))) return rc;
+  if ((rc = check_halo(gp, f->radius))) return rc;
+  const Layout L = layout_of(gp, variant);
+  if (!workspace || workspace_bytes < L.total)
+    return fail(FBF_EINVAL, "bilateral_fast: workspace too small");
+  if (variant == FBF_VARIANT_FUSED && !fused_supported(f->radius)) variant = FBF_VARIANT_NAIVE;
+  if (variant == FBF_VARIANT_NAIVE && workspace_bytes < layout_of(gp, FBF_VARIANT_NAIVE).total)
+    return fail(FBF_EUNSUPPORTED,
+                "bilateral_fast: no fused kernel for this radius and the workspace is too small "
+                "for the naive path");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(workspace);
+  const Layout LV = layout_of(gp, variant);
+  int2* uf = reinterpret_cast<int2*>(ws + LV.uf);
+  Pair* pq = reinterpret_cast<Pair*>(ws + LV.pq);
+
+  Geometry G = to_geometry(gp);
+  Harmonics H;
+  fill_harmonics(H, f);
+  Taps K;
+  fill_taps(K, f);
+
+  // prep writes a dense (batch x src_rows x width) (u, f') image
+  const long long src_px = static_cast<long long>(G.batch) * G.src_rows * G.width;
+  prep_kernel<<<grid_for(src_px, 256), 256, 0, st>>>(src, uf, G, H.turns_per_unit * 4294967296.0,
+                                                     H.shift);
+  FBF_CUDA(cudaGetLastError());
+  Geometry Gd = G;  // dense view of the prep output
+  Gd.src_pitch = G.width;
+  Gd.src_bstride = static_cast<long long>(G.src_rows) * G.width;
+
+  if (variant == FBF_VARIANT_FUSED) {
+    FusedArgs A;
+    std::memset(&A, 0, sizeof(A));
+    A.g = Gd;
+    A.h = H;
+    A.k = K;
+    A.uf = uf;
+    A.dst = dst;
+    A.pq = pq;
+    A.bad = d_bad;
+    A.seg_max = 1 << 30;
+    if (!d_bad) return fail(FBF_EINVAL, "bilateral_fast: the fused path needs a d_bad word");
+    FBF_CUDA(launch_fused(A, st, nullptr));
+    return FBF_OK;
+  }
+
+  // naive: HBM-resident planes
+  float4* M = reinterpret_cast<float4*>(ws + LV.m);
+  float4* T = reinterpret_cast<float4*>(ws + LV.t);
+  float4* C = reinterpret_cast<float4*>(ws + LV.c);
+  NaiveArgs NA;
+  NA.g = Gd;
+  NA.k = K;
+  const long long out_px = static_cast<long long>(G.batch) * G.out_rows * G.width;
+  for (int n = 0; n <= H.N; ++n) {
+    naive_modulate<<<grid_for(src_px, 256), 256, 0, st>>>(uf, M, src_px, static_cast<uint32_t>(n));
+    naive_rows<<<grid_for(src_px, 256), 256, 0, st>>>(M, T, NA);
+    naive_cols<<<grid_for(out_px, 256), 256, 0, st>>>(T, C, NA);
+    naive_demod<<<grid_for(out_px, 256), 256, 0, st>>>(M, C, pq, Gd, H.d[n], n == 0);
+  }
+  finish_kernel<<<grid_for(out_px, 256), 256, 0, st>>>(pq, dst, G, H.shift, H.q_floor, d_bad);
+  FBF_CUDA(cudaGetLastError());
+  return FBF_OK;
+}
+
+int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const float* src,
+                            float* dst, int variant, long long* bad_index) {
+  int rc = check_geometry(g);
+  if (rc) return rc;
+  if ((rc = check_filter(f))) return rc;
+  if ((rc = check_halo(g, f->radius))) return rc;
+  int v = variant;
+  if (v == FBF_VARIANT_FUSED && !fused_supported(f->radius)) v = FBF_VARIANT_NAIVE;
+  // device buffers: dense copies of the source rows and output rows
+  fbf_geometry gd = *g;
+  gd.src_pitch = g->width;
+  gd.dst_pitch = g->width;
+  gd.src_bstride = static_cast<long long>(g->src_rows) * g->width;
+  gd.dst_bstride = static_cast<long long>(g->out_rows) * g->width;
+  const size_t src_bytes = static_cast<size_t>(gd.src_bstride) * g->batch * sizeof(float);
+  const size_t dst_bytes = static_cast<size_t>(gd.dst_bstride) * g->batch * sizeof(float);
+  const size_t ws_bytes = layout_of(&gd, v).total;
+  cudaStream_t st;
+  FBF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  char* buf = nullptr;
+  const size_t total = align256(src_bytes) + align256(dst_bytes) + ws_bytes + 256;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&buf), total, st);
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(st);
+    return cuda_fail(e, "cudaMallocAsync");
+  }
+  float* d_src = reinterpret_cast<float*>(buf);
+  float* d_dst = reinterpret_cast<float*>(buf + align256(src_bytes));
+  void* ws = buf + align256(src_bytes) + align256(dst_bytes);
+  unsigned long long* d_bad =
+      reinterpret_cast<unsigned long long*>(buf + align256(src_bytes) + align256(dst_bytes) + ws_bytes);
+  int out = FBF_OK;
+  do {
+    for (int b = 0; b < g->batch; ++b) {
+      e = cudaMemcpy2DAsync(d_src + b * gd.src_bstride, g->width * sizeof(float),
+                            src + b * g->src_bstride, g->src_pitch * sizeof(float),
+                            g->width * sizeof(float), g->src_rows, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) break;
+    }
+    if (e != cudaSuccess) { out = cuda_fail(e, "H2D"); break; }
+    e = cudaMemsetAsync(d_bad, 0xFF, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) { out = cuda_fail(e, "memset"); break; }
+    out = fbf_bilateral_fast_device(&gd, f, d_src, d_dst, ws, ws_bytes, d_bad, v, st);
+    if (out != FBF_OK) break;
+    for (int b = 0; b < g->batch; ++b) {
+      e = cudaMemcpy2DAsync(dst + b * g->dst_bstride, g->dst_pitch * sizeof(float),
+                            d_dst + b * gd.dst_bstride, g->width * sizeof(float),
+                            g->width * sizeof(float), g->out_rows, cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) break;
+    }
+    if (e != cudaSuccess) { out = cuda_fail(e, "D2H"); break; }
+    unsigned long long bad = ~0ULL;
+    e = cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { out = cuda_fail(e, "sync"); break; }
+    if (bad != ~0ULL) {
+      if (bad_index) *bad_index = static_cast<long long>(bad);
+      const long long per = static_cast<long long>(g->width) * g->height;
+      const long long inimg = static_cast<long long>(bad) % per;
+      const long long x = inimg % g->width, y = inimg / g->width;
+      out = fail(FBF_EANOMALY,
+                 "bilateral_fast: numerical anomaly, denominator collapsed at pixel (" +
+                     std::to_string(x) + ", " + std::to_string(y) + ")");
+    }
+  } while (false);
+  cudaFreeAsync(buf, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  return out;
+}
+
+int fbf_bilateral_fast_host_f64(const fbf_geometry* g, const fbf_filter* f, const double* src,
+                                double* dst, int variant, long long* bad_index) {
+  int rc = check_geometry(g);
+  if (rc) return rc;
+  fbf_geometry gd = *g;
+  gd.src_pitch = g->width;
+  gd.dst_pitch = g->width;
+  gd.src_bstride = static_cast<long long>(g->src_rows) * g->width;
+  gd.dst_bstride = static_cast<long long>(g->out_rows) * g->width;
+  const size_t ns = static_cast<size_t>(gd.src_bstride) * g->batch;
+  const size_t nd = static_cast<size_t>(gd.dst_bstride) * g->batch;
+  float* hs = nullptr;
+  float* hd = nullptr;
+  FBF_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hs), ns * sizeof(float)));
+  cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&hd), nd * sizeof(float));
+  if (e != cudaSuccess) {
+    cudaFreeHost(hs);
+    return cuda_fail(e, "cudaMallocHost");
+  }
+  for (int b = 0; b < g->batch; ++b)
+    for (int y = 0; y < g->src_rows; ++y)
+      for (int x = 0; x < g->width; ++x)
+        hs[b * gd.src_bstride + static_cast<long long>(y) * g->width + x] =
+            static_cast<float>(src[b * g->src_bstride + y * g->src_pitch + x]);
+  rc = fbf_bilateral_fast_host(&gd, f, hs, hd, variant, bad_index);
+  if (rc == FBF_OK)
+    for (int b = 0; b < g->batch; ++b)
+      for (int y = 0; y < g->out_rows; ++y)
+        for (int x = 0; x < g->width; ++x)
+          dst[b * g->dst_bstride + y * g->dst_pitch + x] =
+              hd[b * gd.dst_bstride + static_cast<long long>(y) * g->width + x];
+  cudaFreeHost(hs);
+  cudaFreeHost(hd);
+  return rc;
+}
+
+int fbf_convolve_device(int width, int height, const double* profile, int radius, const float* src,
+                        float* dst, void* workspace, size_t workspace_bytes, void* stream) {
+  if (width <= 0 || height <= 0) return fail(FBF_EINVAL, "convolve: empty plane");
+  if (radius < 0 || radius > kMaxW) return fail(FBF_EUNSUPPORTED, "convolve: radius outside [0, 64]");
+  const size_t need = static_cast<size_t>(width) * height * sizeof(float);
+  if (!workspace || workspace_bytes < need) return fail(FBF_EINVAL, "convolve: workspace too small");
+  Taps K;
+  std::memset(&K, 0, sizeof(K));
+  K.W = radius;
+  for (int j = 0; j <= radius; ++j) {
+    K.t[j] = static_cast<float>(profile[radius + j]);
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* tmp = static_cast<float*>(workspace);
+  const long long n = static_cast<long long>(width) * height;
+  conv_rows_f32<<<grid_for(n, 256), 256, 0, st>>>(src, tmp, width, height, K);
+  conv_cols_f32<<<grid_for(n, 256), 256, 0, st>>>(tmp, dst, width, height, K);
+  FBF_CUDA(cudaGetLastError());
+  return FBF_OK;
+}
+
+int fbf_convolve_host_f64(int width, int height, const double* profile, int radius,
+                          const double* src, double* dst) {
+  if (width <= 0 || height <= 0) return fail(FBF_EINVAL, "convolve: empty plane");
+  const size_t n = static_cast<size_t>(width) * height;
+  cudaStream_t st;
+  FBF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  float* h = nullptr;
+  char* d = nullptr;
+  cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&h), n * sizeof(float));
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&d), 3 * align256(n * 4), st);
+  int rc = FBF_OK;
+  if (e != cudaSuccess) {
+    rc = cuda_fail(e, "alloc");
+  } else {
+    for (size_t i = 0; i < n; ++i) h[i] = static_cast<float>(src[i]);
+    float* ds = reinterpret_cast<float*>(d);
+    float* dd = reinterpret_cast<float*>(d + align256(n * 4));
+    void* ws = d + 2 * align256(n * 4);
+    e = cudaMemcpyAsync(ds, h, n * 4, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+      rc = fbf_convolve_device(width, height, profile, radius, ds, dd, ws, align256(n * 4), st);
+      if (rc == FBF_OK) {
+        e = cudaMemcpyAsync(h, dd, n * 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) rc = cuda_fail(e, "convolve D2H");
+        else
+          for (size_t i = 0; i < n; ++i) dst[i] = h[i];
+      }
+    } else {
+      rc = cuda_fail(e, "convolve H2D");
+    }
+    cudaFreeAsync(d, st);
+  }
+  cudaStreamSynchronize(st);
+  if (h) cudaFreeHost(h);
+  cudaStreamDestroy(st);
+  return rc;
+}
+
+int fbf_probe_fma_peak(double* ops_per_s, double* sm_mhz, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int dev = 0, sms = 0;
+  FBF_CUDA(cudaGetDevice(&dev));
+  FBF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int blocks = sms * 4, threads = 256, iters = 40000;
+  float* out = nullptr;
+  long long* cyc = nullptr;
+  FBF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&out), blocks * threads * sizeof(float), st));
+  FBF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cyc), blocks * sizeof(long long), st));
+  fma_probe<<<blocks, threads, 0, st>>>(out, 1.0001f, 0.5f, 200, cyc);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  fma_probe<<<blocks, threads, 0, st>>>(out, 1.0001f, 0.5f, iters, cyc);
+  cudaEventRecord(e1, st);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  long long* h = new long long[blocks];
+  cudaMemcpyAsync(h, cyc, blocks * sizeof(long long), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  long long mx = 0;
+  for (int i = 0; i < blocks; ++i) mx = std::max(mx, h[i]);
+  delete[] h;
+  cudaFreeAsync(out, st);
+  cudaFreeAsync(cyc, st);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  FBF_CUDA(cudaStreamSynchronize(st));
+  const double ops = static_cast<double>(blocks) * threads * iters * 16.0;
+  if (ops_per_s) *ops_per_s = ops / (ms * 1e-3);
+  if (sm_mhz) *sm_mhz = static_cast<double>(mx) / (ms * 1e3);
+  return FBF_OK;
+}
+
+}  // extern "C"

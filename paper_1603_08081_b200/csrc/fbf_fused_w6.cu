@@ -1,0 +1,3 @@
+// fused kernel instantiation for spatial radius W=6 (one TU per radius: parallel builds)
+#include "fbf_fused.cuh"
+FBF_INSTANTIATE_FUSED(6)

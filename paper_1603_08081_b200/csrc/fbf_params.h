@@ -1,0 +1,59 @@
+// fbf_params.h -- launch parameter blocks (passed by value: they live in the
+// kernel's constant bank, so taps and coefficients are uniform operands).
+#pragma once
+#include <cstdint>
+
+namespace fbf {
+
+constexpr int kMaxN = 127;  // highest harmonic supported by one launch
+constexpr int kMaxW = 64;   // largest spatial radius supported by the fused/naive paths
+
+struct Pair {
+  float x, y;
+};
+
+// Geometry shared by every kernel that reads a (possibly strip-local,
+// possibly batched) image.  Global image is width x full_height; the device
+// buffer holds global rows [src_row0, src_row0 + src_rows) of each image;
+// output rows [out_row0, out_row0 + out_rows) are produced.
+struct Geometry {
+  int width;
+  int full_height;
+  int src_row0, src_rows;
+  int out_row0, out_rows;
+  int batch;
+  long long src_bstride;  // elements between images in the source / uf buffers
+  int src_pitch;          // elements between rows of the source buffer
+  long long dst_bstride;  // elements between images in dst
+  int dst_pitch;          // elements between rows of dst (row 0 = global out_row0)
+};
+
+struct Harmonics {
+  int N;
+  float d[kMaxN + 1];  // cosine coefficients d_0..d_N (fp32)
+  double turns_per_unit;  // omega / (2 pi): phase in turns per intensity unit
+  float shift;            // intensity shift applied before modulation (128)
+  float q_floor;          // (w0 - eps) / 2 : denominator collapse threshold
+};
+
+struct Taps {
+  int W;
+  int box;                // 1: uniform box window (running-sum path)
+  float box_tap;          // 1/(2W+1)
+  float t[kMaxW + 1];     // tap |j| (spatial.hpp profile[W+j]); broadcast to both FFMA2 lanes
+};
+
+struct FusedArgs {
+  Geometry g;
+  Harmonics h;
+  Taps k;
+  const int2* uf;          // prep output: (u = phase increment, f' bits)
+  float* dst;
+  Pair* pq;                // workspace: per output pixel (Q, P), out_rows x width per image
+  unsigned long long* bad; // min linear index (b*H*W + y*W + x) of a collapsed denominator
+  int strips;              // ceil(width / TW)
+  long long total;         // batch * strips * out_rows
+  int seg_max;             // longest row run one CTA filters in one pass over n
+};
+
+}  // namespace fbf
