@@ -72,8 +72,8 @@ int fbf_version(void);
 /* Fills g for a whole single image (or a batch of contiguous images). */
 void fbf_geometry_whole(fbf_geometry* g, int width, int height, int batch);
 
-/* Device workspace needed by fbf_bilateral_fast_device (bytes). */
-size_t fbf_workspace_bytes(const fbf_geometry* g, int variant);
+/* Device workspace needed by fbf_bilateral_fast_device for spatial radius W (bytes). */
+size_t fbf_workspace_bytes(const fbf_geometry* g, int radius, int variant);
 
 /* Asynchronous, device-resident: src/dst/workspace are device pointers,
  * `stream` a cudaStream_t (NULL = legacy default).  d_bad (device, may be
@@ -82,6 +82,17 @@ size_t fbf_workspace_bytes(const fbf_geometry* g, int variant);
 int fbf_bilateral_fast_device(const fbf_geometry* g, const fbf_filter* f, const float* src,
                               float* dst, void* workspace, size_t workspace_bytes,
                               unsigned long long* d_bad, int variant, void* stream);
+
+/* The two stages of fbf_bilateral_fast_device, for callers that time or
+ * overlap them separately: (1) the per-pixel base phase u = round(f' omega/2pi
+ * 2^32) and f' = f - 128 into the workspace; (2) the filter proper. */
+int fbf_prepare_device(const fbf_geometry* g, const fbf_filter* f, const float* src,
+                       void* workspace, size_t workspace_bytes, int variant, void* stream);
+int fbf_filter_prepared_device(const fbf_geometry* g, const fbf_filter* f, float* dst,
+                               void* workspace, size_t workspace_bytes,
+                               unsigned long long* d_bad, int variant, void* stream);
+/* Kernel launches one fbf_bilateral_fast_device call makes. */
+int fbf_launches_per_call(const fbf_filter* f, int variant);
 
 /* Synchronous, host buffers (fp32): H2D, filter, D2H.  On FBF_EANOMALY
  * *bad_index holds the first offending index. */

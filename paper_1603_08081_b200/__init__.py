@@ -57,9 +57,14 @@ SIGNATURES = {
     "fbf_last_error": (ctypes.c_char_p, []),
     "fbf_version": (ctypes.c_int, []),
     "fbf_geometry_whole": (None, [ctypes.POINTER(Geometry), ctypes.c_int, ctypes.c_int, ctypes.c_int]),
-    "fbf_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(Geometry), ctypes.c_int]),
+    "fbf_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(Geometry), ctypes.c_int, ctypes.c_int]),
     "fbf_bilateral_fast_device": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.POINTER(Filter), _P, _P, _P,
                                                  ctypes.c_size_t, _P, ctypes.c_int, _P]),
+    "fbf_prepare_device": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.POINTER(Filter), _P, _P,
+                                          ctypes.c_size_t, ctypes.c_int, _P]),
+    "fbf_filter_prepared_device": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.POINTER(Filter), _P, _P,
+                                                  ctypes.c_size_t, _P, ctypes.c_int, _P]),
+    "fbf_launches_per_call": (ctypes.c_int, [ctypes.POINTER(Filter), ctypes.c_int]),
     "fbf_bilateral_fast_host": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.POINTER(Filter), _F, _F,
                                                ctypes.c_int, _LL]),
     "fbf_bilateral_fast_host_f64": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.POINTER(Filter), _D, _D,
@@ -258,8 +263,31 @@ def bilateral_fast_device(src_ptr: int, dst_ptr: int, geometry: Geometry, spatia
                                          workspace_ptr, workspace_bytes, bad_ptr, _VARIANTS[variant], stream))
 
 
-def workspace_bytes(geometry: Geometry, variant: str = "fused") -> int:
-    return int(lib.fbf_workspace_bytes(ctypes.byref(geometry), _VARIANTS[variant]))
+def prepare_device(src_ptr: int, geometry: Geometry, spatial: SpatialKernel, approx: FourierKernelApprox,
+                   workspace_ptr: int, workspace_bytes: int, stream: int = 0, variant: str = "fused",
+                   check_epsilon: bool = True) -> None:
+    """Stage 1 of bilateral_fast_device: base phase + shifted intensity into the workspace."""
+    f = _filter_struct(spatial, approx, check_epsilon)
+    _check(lib.fbf_prepare_device(ctypes.byref(geometry), ctypes.byref(f), src_ptr, workspace_ptr,
+                                  workspace_bytes, _VARIANTS[variant], stream))
+
+
+def filter_prepared_device(dst_ptr: int, geometry: Geometry, spatial: SpatialKernel, approx: FourierKernelApprox,
+                           workspace_ptr: int, workspace_bytes: int, bad_ptr: int, stream: int = 0,
+                           variant: str = "fused", check_epsilon: bool = True) -> None:
+    """Stage 2 of bilateral_fast_device: the filter proper (fused kernel or the naive chain)."""
+    f = _filter_struct(spatial, approx, check_epsilon)
+    _check(lib.fbf_filter_prepared_device(ctypes.byref(geometry), ctypes.byref(f), dst_ptr, workspace_ptr,
+                                          workspace_bytes, bad_ptr, _VARIANTS[variant], stream))
+
+
+def launches_per_call(spatial: SpatialKernel, approx: FourierKernelApprox, variant: str = "fused") -> int:
+    f = _filter_struct(spatial, approx)
+    return int(lib.fbf_launches_per_call(ctypes.byref(f), _VARIANTS[variant]))
+
+
+def workspace_bytes(geometry: Geometry, radius: int, variant: str = "fused") -> int:
+    return int(lib.fbf_workspace_bytes(ctypes.byref(geometry), int(radius), _VARIANTS[variant]))
 
 
 def convolve(plane: np.ndarray, spatial: SpatialKernel) -> np.ndarray:

@@ -64,6 +64,29 @@ __global__ void prep_kernel(const float* __restrict__ src, int2* __restrict__ uf
   }
 }
 
+// fused path: the same (u, f') on a mirror-padded grid, rows = global rows
+// [out_row0 - W, out_row0 + out_rows + W), columns = global [-W, cols + W)
+// with cols = strips * TW, so every TMA tile of the fused kernel is in bounds.
+__global__ void prep_padded_kernel(const float* __restrict__ src, int2* __restrict__ uf, Geometry g,
+                                   int W, int cols, double turns_scaled, float shift) {
+  const int pw = cols + 2 * W, ph = g.out_rows + 2 * W;
+  const long long per = static_cast<long long>(ph) * pw;
+  const long long total = per * g.batch;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long b = i / per;
+    const long long r = i - b * per;
+    const int py = static_cast<int>(r / pw);
+    const int px = static_cast<int>(r - static_cast<long long>(py) * pw);
+    const int gy = mirror_index(g.out_row0 - W + py, g.full_height) - g.src_row0;
+    const int gx = mirror_index(px - W, g.width);
+    const float f = src[b * g.src_bstride + static_cast<long long>(gy) * g.src_pitch + gx];
+    const double fd = static_cast<double>(f) - static_cast<double>(shift);
+    const long long u = __double2ll_rn(fd * turns_scaled);
+    uf[i] = make_int2(static_cast<int>(static_cast<unsigned>(u)), __float_as_int(static_cast<float>(fd)));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // naive variant: per harmonic four kernels over HBM-resident float4 planes
 //   modulate -> row FIR -> column FIR -> demodulate, then one divide kernel.
@@ -73,7 +96,7 @@ struct NaiveArgs {
   Taps k;
 };
 
-__global__ void naive_modulate(const int2* __restrict__ uf, float4* __restrict__ M, long long total,
+__global__ void naive_modulate(const int2* __restrict__ uf, ulonglong2* __restrict__ M, long long total,
                                uint32_t n) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -81,11 +104,11 @@ __global__ void naive_modulate(const int2* __restrict__ uf, float4* __restrict__
     float c, s;
     sincos_turns(n * static_cast<uint32_t>(v.x), c, s);
     const float fp = __int_as_float(v.y);
-    M[i] = make_float4(c, c * fp, s, s * fp);
+    M[i] = make_ulonglong2(pk(c, c * fp), pk(s, s * fp));
   }
 }
 
-__global__ void naive_rows(const float4* __restrict__ in, float4* __restrict__ out,
+__global__ void naive_rows(const ulonglong2* __restrict__ in, ulonglong2* __restrict__ out,
                            const __grid_constant__ NaiveArgs a) {
   const long long per = static_cast<long long>(a.g.src_rows) * a.g.width;
   const long long total = per * a.g.batch;
@@ -94,20 +117,18 @@ __global__ void naive_rows(const float4* __restrict__ in, float4* __restrict__ o
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long rowbase = i - (i % a.g.width);
     const int x = static_cast<int>(i % a.g.width);
-    f2 A{0.f, 0.f}, B{0.f, 0.f};
+    p2 A = 0, B = 0;
     for (int j = -W; j <= W; ++j) {  // out(x) = sum_j p[j] in(x - j), spatial.hpp:82-86
-      const float4 v = in[rowbase + mirror_index(x - j, a.g.width)];
-      const int tj = j < 0 ? -j : j;
-      const float tv = a.k.t[tj];
-      const f2 t{tv, tv};
-      ffma2(A, t, f2{v.x, v.y});
-      ffma2(B, t, f2{v.z, v.w});
+      const ulonglong2 v = in[rowbase + mirror_index(x - j, a.g.width)];
+      const float tv = a.k.t[j < 0 ? -j : j];
+      A = fma2(pk(tv, tv), v.x, A);
+      B = fma2(pk(tv, tv), v.y, B);
     }
-    out[i] = make_float4(A.x, A.y, B.x, B.y);
+    out[i] = make_ulonglong2(A, B);
   }
 }
 
-__global__ void naive_cols(const float4* __restrict__ in, float4* __restrict__ out,
+__global__ void naive_cols(const ulonglong2* __restrict__ in, ulonglong2* __restrict__ out,
                            const __grid_constant__ NaiveArgs a) {
   const long long per_out = static_cast<long long>(a.g.out_rows) * a.g.width;
   const long long per_src = static_cast<long long>(a.g.src_rows) * a.g.width;
@@ -119,23 +140,21 @@ __global__ void naive_cols(const float4* __restrict__ in, float4* __restrict__ o
     const long long r = i - b * per_out;
     const int y = a.g.out_row0 + static_cast<int>(r / a.g.width);
     const int x = static_cast<int>(r % a.g.width);
-    const float4* src = in + b * per_src;
-    f2 A{0.f, 0.f}, B{0.f, 0.f};
+    const ulonglong2* src = in + b * per_src;
+    p2 A = 0, B = 0;
     for (int j = -W; j <= W; ++j) {
       const int sy = mirror_index(y - j, a.g.full_height) - a.g.src_row0;
-      const float4 v = src[static_cast<long long>(sy) * a.g.width + x];
-      const int tj = j < 0 ? -j : j;
-      const float tv = a.k.t[tj];
-      const f2 t{tv, tv};
-      ffma2(A, t, f2{v.x, v.y});
-      ffma2(B, t, f2{v.z, v.w});
+      const ulonglong2 v = src[static_cast<long long>(sy) * a.g.width + x];
+      const float tv = a.k.t[j < 0 ? -j : j];
+      A = fma2(pk(tv, tv), v.x, A);
+      B = fma2(pk(tv, tv), v.y, B);
     }
-    out[i] = make_float4(A.x, A.y, B.x, B.y);
+    out[i] = make_ulonglong2(A, B);
   }
 }
 
-__global__ void naive_demod(const float4* __restrict__ M, const float4* __restrict__ C,
-                            Pair* __restrict__ pq, Geometry g, float dn, int first) {
+__global__ void naive_demod(const ulonglong2* __restrict__ M, const ulonglong2* __restrict__ C,
+                            p2* __restrict__ pq, Geometry g, float dn, int first) {
   const long long per_out = static_cast<long long>(g.out_rows) * g.width;
   const long long per_src = static_cast<long long>(g.src_rows) * g.width;
   const long long total = per_out * g.batch;
@@ -145,16 +164,16 @@ __global__ void naive_demod(const float4* __restrict__ M, const float4* __restri
     const long long r = i - b * per_out;
     const int y = g.out_row0 + static_cast<int>(r / g.width);
     const int x = static_cast<int>(r % g.width);
-    const float4 m = M[b * per_src + static_cast<long long>(y - g.src_row0) * g.width + x];
-    const float4 c = C[i];
-    f2 qp = mul2(f2{m.x, m.x}, f2{c.x, c.y});
-    qp = fma2(f2{m.z, m.z}, f2{c.z, c.w}, qp);
-    f2 acc = first ? mul2(f2{dn, dn}, qp) : fma2(f2{dn, dn}, qp, f2{pq[i].x, pq[i].y});
-    pq[i] = Pair{acc.x, acc.y};
+    const ulonglong2 m = M[b * per_src + static_cast<long long>(y - g.src_row0) * g.width + x];
+    const ulonglong2 c = C[i];
+    const float cc = lo_of(m.x), ss = lo_of(m.y);
+    p2 qp = mul2(pk(cc, cc), c.x);  // (c Gc, c Fc) + (s Gs, s Fs)
+    qp = fma2(pk(ss, ss), c.y, qp);
+    pq[i] = first ? mul2(pk(dn, dn), qp) : fma2(pk(dn, dn), qp, pq[i]);
   }
 }
 
-__global__ void finish_kernel(const Pair* __restrict__ pq, float* __restrict__ dst, Geometry g,
+__global__ void finish_kernel(const p2* __restrict__ pq, float* __restrict__ dst, Geometry g,
                               float shift, float q_floor, unsigned long long* bad) {
   const long long per_out = static_cast<long long>(g.out_rows) * g.width;
   const long long total = per_out * g.batch;
@@ -164,13 +183,14 @@ __global__ void finish_kernel(const Pair* __restrict__ pq, float* __restrict__ d
     const long long r = i - b * per_out;
     const int yl = static_cast<int>(r / g.width);
     const int x = static_cast<int>(r % g.width);
-    const Pair v = pq[i];
-    if (!(fabsf(v.x) >= q_floor) && bad) {
+    float Q, P;
+    upk(pq[i], Q, P);
+    if (!(fabsf(Q) >= q_floor) && bad) {
       const unsigned long long lin = static_cast<unsigned long long>(b) * g.full_height * g.width +
                                      static_cast<unsigned long long>(g.out_row0 + yl) * g.width + x;
       atomicMin(bad, lin);
     }
-    dst[b * g.dst_bstride + static_cast<long long>(yl) * g.dst_pitch + x] = shift + __fdiv_rn(v.y, v.x);
+    dst[b * g.dst_bstride + static_cast<long long>(yl) * g.dst_pitch + x] = shift + __fdiv_rn(P, Q);
   }
 }
 
@@ -209,10 +229,10 @@ __global__ void conv_cols_f32(const float* __restrict__ in, float* __restrict__ 
 
 __global__ void __launch_bounds__(256) fma_probe(float* out, float a, float b, int iters,
                                                  long long* cycles) {
-  f2 acc[8];
+  p2 acc[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) acc[i] = f2{threadIdx.x * 1e-3f + i, static_cast<float>(i)};
-  const f2 ma{a, a}, mb{b, b};
+  for (int i = 0; i < 8; ++i) acc[i] = pk(threadIdx.x * 1e-3f + i, static_cast<float>(i));
+  const p2 ma = pk(a, a), mb = pk(b, b);
   const long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
@@ -221,7 +241,7 @@ __global__ void __launch_bounds__(256) fma_probe(float* out, float a, float b, i
   const long long t1 = clock64();
   float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) s += acc[i].x + acc[i].y;
+  for (int i = 0; i < 8; ++i) s += lo_of(acc[i]) + hi_of(acc[i]);
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
   if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
 }
@@ -312,14 +332,24 @@ struct Layout {
   size_t uf, pq, m, t, c, total;
 };
 
-Layout layout_of(const fbf_geometry* g, int variant) {
+// Fused: mirror-padded (u, f') image (out_rows + 2W) x (strips*TW + 2W) and a
+// (Q, P) plane out_rows x strips*TW per image (see FusedArgs).  Naive: dense
+// (u, f') of the source rows, (Q, P) per output pixel and three float4 planes.
+Layout layout_of(const fbf_geometry* g, int radius, int variant) {
   Layout L{};
   const size_t src_px = static_cast<size_t>(g->batch) * g->src_rows * g->width;
   const size_t out_px = static_cast<size_t>(g->batch) * g->out_rows * g->width;
   L.uf = 0;
+  if (variant == FBF_VARIANT_FUSED) {
+    const size_t cols = static_cast<size_t>((g->width + kFusedTW - 1) / kFusedTW) * kFusedTW;
+    const size_t uf_px = static_cast<size_t>(g->batch) * (g->out_rows + 2 * radius) * (cols + 2 * radius);
+    L.pq = align256(uf_px * sizeof(int2));
+    L.total = L.pq + align256(static_cast<size_t>(g->batch) * g->out_rows * cols * sizeof(Pair));
+    return L;
+  }
   L.pq = align256(src_px * sizeof(int2));
   size_t end = L.pq + align256(out_px * sizeof(Pair));
-  if (variant == FBF_VARIANT_NAIVE) {
+  {
     L.m = end;
     L.t = L.m + align256(src_px * sizeof(float4));
     L.c = L.t + align256(src_px * sizeof(float4));
@@ -350,80 +380,126 @@ void fbf_geometry_whole(fbf_geometry* g, int width, int height, int batch) {
   g->dst_bstride = static_cast<long long>(width) * height;
 }
 
-size_t fbf_workspace_bytes(const fbf_geometry* g, int variant) {
-  if (check_geometry(g) != FBF_OK) return 0;
-  return layout_of(g, variant).total;
+size_t fbf_workspace_bytes(const fbf_geometry* g, int radius, int variant) {
+  if (check_geometry(g) != FBF_OK || radius < 1 || radius > kMaxW) return 0;
+  if (variant == FBF_VARIANT_FUSED && !fused_supported(radius)) variant = FBF_VARIANT_NAIVE;
+  return layout_of(g, radius, variant).total;
+}
+
+namespace {
+
+struct Prepared {
+  Geometry G, Gd;
+  Harmonics H;
+  Taps K;
+  int variant;
+  int2* uf;
+  Pair* pq;
+  char* ws;
+  Layout L;
+};
+
+int prepare_common(const fbf_geometry* gp, const fbf_filter* f, void* workspace,
+                   size_t workspace_bytes, int variant, Prepared& P) {
+  int rc = check_geometry(gp);
+  if (rc) return rc;
+  if ((rc = check_filter(f))) return rc;
+  if ((rc = check_halo(gp, f->radius))) return rc;
+  if (variant == FBF_VARIANT_FUSED && !fused_supported(f->radius)) variant = FBF_VARIANT_NAIVE;
+  P.L = layout_of(gp, f->radius, variant);
+  if (!workspace || workspace_bytes < P.L.total)
+    return fail(FBF_EINVAL, variant == FBF_VARIANT_NAIVE
+                                ? "bilateral_fast: workspace too small for the naive path (no fused "
+                                  "kernel is compiled for this radius)"
+                                : "bilateral_fast: workspace too small");
+  P.variant = variant;
+  P.ws = static_cast<char*>(workspace);
+  P.uf = reinterpret_cast<int2*>(P.ws + P.L.uf);
+  P.pq = reinterpret_cast<Pair*>(P.ws + P.L.pq);
+  P.G = to_geometry(gp);
+  fill_harmonics(P.H, f);
+  fill_taps(P.K, f);
+  P.Gd = P.G;  // dense view of the prep output: batch x src_rows x width
+  P.Gd.src_pitch = P.G.width;
+  P.Gd.src_bstride = static_cast<long long>(P.G.src_rows) * P.G.width;
+  return FBF_OK;
+}
+
+}  // namespace
+
+int fbf_prepare_device(const fbf_geometry* gp, const fbf_filter* f, const float* src,
+                       void* workspace, size_t workspace_bytes, int variant, void* stream) {
+  Prepared P;
+  int rc = prepare_common(gp, f, workspace, workspace_bytes, variant, P);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const double scale = P.H.turns_per_unit * 4294967296.0;
+  if (P.variant == FBF_VARIANT_FUSED) {
+    const int W = f->radius;
+    const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
+    const long long n = static_cast<long long>(P.G.batch) * (P.G.out_rows + 2 * W) * (cols + 2 * W);
+    prep_padded_kernel<<<grid_for(n, 256), 256, 0, st>>>(src, P.uf, P.G, W, cols, scale, P.H.shift);
+  } else {
+    const long long src_px = static_cast<long long>(P.G.batch) * P.G.src_rows * P.G.width;
+    prep_kernel<<<grid_for(src_px, 256), 256, 0, st>>>(src, P.uf, P.G, scale, P.H.shift);
+  }
+  FBF_CUDA(cudaGetLastError());
+  return FBF_OK;
+}
+
+int fbf_filter_prepared_device(const fbf_geometry* gp, const fbf_filter* f, float* dst,
+                               void* workspace, size_t workspace_bytes, unsigned long long* d_bad,
+                               int variant, void* stream) {
+  Prepared P;
+  int rc = prepare_common(gp, f, workspace, workspace_bytes, variant, P);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (P.variant == FBF_VARIANT_FUSED) {
+    FusedArgs A;
+    std::memset(&A, 0, sizeof(A));
+    A.g = P.Gd;
+    A.h = P.H;
+    A.k = P.K;
+    A.uf = P.uf;
+    A.dst = dst;
+    A.pq = P.pq;
+    A.bad = d_bad;
+    A.seg_max = 1 << 30;
+    FBF_CUDA(launch_fused(A, st, nullptr));
+    return FBF_OK;
+  }
+  // naive: HBM-resident planes, four kernels per harmonic
+  ulonglong2* M = reinterpret_cast<ulonglong2*>(P.ws + P.L.m);
+  ulonglong2* T = reinterpret_cast<ulonglong2*>(P.ws + P.L.t);
+  ulonglong2* C = reinterpret_cast<ulonglong2*>(P.ws + P.L.c);
+  NaiveArgs NA;
+  NA.g = P.Gd;
+  NA.k = P.K;
+  const long long src_px = static_cast<long long>(P.G.batch) * P.G.src_rows * P.G.width;
+  const long long out_px = static_cast<long long>(P.G.batch) * P.G.out_rows * P.G.width;
+  for (int n = 0; n <= P.H.N; ++n) {
+    naive_modulate<<<grid_for(src_px, 256), 256, 0, st>>>(P.uf, M, src_px, static_cast<uint32_t>(n));
+    naive_rows<<<grid_for(src_px, 256), 256, 0, st>>>(M, T, NA);
+    naive_cols<<<grid_for(out_px, 256), 256, 0, st>>>(T, C, NA);
+    naive_demod<<<grid_for(out_px, 256), 256, 0, st>>>(M, C, reinterpret_cast<p2*>(P.pq), P.Gd, P.H.d[n], n == 0);
+  }
+  finish_kernel<<<grid_for(out_px, 256), 256, 0, st>>>(reinterpret_cast<p2*>(P.pq), dst, P.G, P.H.shift, P.H.q_floor, d_bad);
+  FBF_CUDA(cudaGetLastError());
+  return FBF_OK;
 }
 
 int fbf_bilateral_fast_device(const fbf_geometry* gp, const fbf_filter* f, const float* src,
                               float* dst, void* workspace, size_t workspace_bytes,
                               unsigned long long* d_bad, int variant, void* stream) {
-  int rc = check_geometry(gp);
+  int rc = fbf_prepare_device(gp, f, src, workspace, workspace_bytes, variant, stream);
   if (rc) return rc;
-  if ((rc = check_filter(f))) return rc;
-  if ((rc = check_halo(gp, f->radius))) return rc;
-  const Layout L = layout_of(gp, variant);
-  if (!workspace || workspace_bytes < L.total)
-    return fail(FBF_EINVAL, "bilateral_fast: workspace too small");
-  if (variant == FBF_VARIANT_FUSED && !fused_supported(f->radius)) variant = FBF_VARIANT_NAIVE;
-  if (variant == FBF_VARIANT_NAIVE && workspace_bytes < layout_of(gp, FBF_VARIANT_NAIVE).total)
-    return fail(FBF_EUNSUPPORTED,
-                "bilateral_fast: no fused kernel for this radius and the workspace is too small "
-                "for the naive path");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  char* ws = static_cast<char*>(workspace);
-  const Layout LV = layout_of(gp, variant);
-  int2* uf = reinterpret_cast<int2*>(ws + LV.uf);
-  Pair* pq = reinterpret_cast<Pair*>(ws + LV.pq);
+  return fbf_filter_prepared_device(gp, f, dst, workspace, workspace_bytes, d_bad, variant, stream);
+}
 
-  Geometry G = to_geometry(gp);
-  Harmonics H;
-  fill_harmonics(H, f);
-  Taps K;
-  fill_taps(K, f);
-
-  // prep writes a dense (batch x src_rows x width) (u, f') image
-  const long long src_px = static_cast<long long>(G.batch) * G.src_rows * G.width;
-  prep_kernel<<<grid_for(src_px, 256), 256, 0, st>>>(src, uf, G, H.turns_per_unit * 4294967296.0,
-                                                     H.shift);
-  FBF_CUDA(cudaGetLastError());
-  Geometry Gd = G;  // dense view of the prep output
-  Gd.src_pitch = G.width;
-  Gd.src_bstride = static_cast<long long>(G.src_rows) * G.width;
-
-  if (variant == FBF_VARIANT_FUSED) {
-    FusedArgs A;
-    std::memset(&A, 0, sizeof(A));
-    A.g = Gd;
-    A.h = H;
-    A.k = K;
-    A.uf = uf;
-    A.dst = dst;
-    A.pq = pq;
-    A.bad = d_bad;
-    A.seg_max = 1 << 30;
-    if (!d_bad) return fail(FBF_EINVAL, "bilateral_fast: the fused path needs a d_bad word");
-    FBF_CUDA(launch_fused(A, st, nullptr));
-    return FBF_OK;
-  }
-
-  // naive: HBM-resident planes
-  float4* M = reinterpret_cast<float4*>(ws + LV.m);
-  float4* T = reinterpret_cast<float4*>(ws + LV.t);
-  float4* C = reinterpret_cast<float4*>(ws + LV.c);
-  NaiveArgs NA;
-  NA.g = Gd;
-  NA.k = K;
-  const long long out_px = static_cast<long long>(G.batch) * G.out_rows * G.width;
-  for (int n = 0; n <= H.N; ++n) {
-    naive_modulate<<<grid_for(src_px, 256), 256, 0, st>>>(uf, M, src_px, static_cast<uint32_t>(n));
-    naive_rows<<<grid_for(src_px, 256), 256, 0, st>>>(M, T, NA);
-    naive_cols<<<grid_for(out_px, 256), 256, 0, st>>>(T, C, NA);
-    naive_demod<<<grid_for(out_px, 256), 256, 0, st>>>(M, C, pq, Gd, H.d[n], n == 0);
-  }
-  finish_kernel<<<grid_for(out_px, 256), 256, 0, st>>>(pq, dst, G, H.shift, H.q_floor, d_bad);
-  FBF_CUDA(cudaGetLastError());
-  return FBF_OK;
+int fbf_launches_per_call(const fbf_filter* f, int variant) {
+  if (!f) return 0;
+  if (variant == FBF_VARIANT_FUSED && fused_supported(f->radius)) return 2;
+  return 1 + 4 * (f->N + 1) + 1;
 }
 
 int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const float* src,
@@ -442,7 +518,7 @@ int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const fl
   gd.dst_bstride = static_cast<long long>(g->out_rows) * g->width;
   const size_t src_bytes = static_cast<size_t>(gd.src_bstride) * g->batch * sizeof(float);
   const size_t dst_bytes = static_cast<size_t>(gd.dst_bstride) * g->batch * sizeof(float);
-  const size_t ws_bytes = layout_of(&gd, v).total;
+  const size_t ws_bytes = layout_of(&gd, f->radius, v).total;
   cudaStream_t st;
   FBF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   char* buf = nullptr;

@@ -8,41 +8,92 @@
 //    be carried between harmonics.
 //  * sincos_turns: quadrant reduction + paired minimax polynomials evaluated with
 //    FFMA2 (fma.rn.f32x2), ~1 ulp, no MUFU and no table (no bank conflicts).
-//  * ffma2: the Blackwell paired FP32 FMA; two fp32 lanes per instruction halves
-//    the issue pressure of the FIR inner loops (measured: FFMA and FFMA2 both
-//    reach ~126 lane-ops/clk/SM, profiles/r01_fma_microbench.txt).
+//  * pairs: two fp32 lanes in one 64-bit register pair (p2).  Blackwell's FFMA2
+//    does both lanes in one instruction, halving the issue pressure of the FIR
+//    loops (measured: FFMA and FFMA2 both reach ~126 lane-ops/clk/SM,
+//    profiles/r01_fma_microbench.txt).  A pair built from one scalar {t, t}
+//    compiles to FFMA2's scalar-broadcast operand form (no register moves).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace fbf {
 
-struct f2 {
-  float x, y;
-};
+using p2 = unsigned long long;  // packed (lo, hi) fp32 pair
 
-__device__ __forceinline__ unsigned long long as_u64(f2 v) {
-  return (static_cast<unsigned long long>(__float_as_uint(v.y)) << 32) | __float_as_uint(v.x);
+__device__ __forceinline__ p2 pk(float lo, float hi) {
+  p2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
 }
-__device__ __forceinline__ f2 as_f2(unsigned long long u) {
-  return f2{__uint_as_float(static_cast<unsigned>(u)), __uint_as_float(static_cast<unsigned>(u >> 32))};
+__device__ __forceinline__ void upk(p2 v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ float lo_of(p2 v) {
+  float a, b;
+  upk(v, a, b);
+  return a;
+}
+__device__ __forceinline__ float hi_of(p2 v) {
+  float a, b;
+  upk(v, a, b);
+  return b;
+}
+// a * b + c, lane-wise
+__device__ __forceinline__ p2 fma2(p2 a, p2 b, p2 c) {
+  p2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ p2 mul2(p2 a, p2 b) {
+  p2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
 }
 
-// acc += a * b, lane-wise on the pair
-__device__ __forceinline__ void ffma2(f2& acc, f2 a, f2 b) {
-  unsigned long long r = as_u64(acc);
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(r) : "l"(as_u64(a)), "l"(as_u64(b)));
-  acc = as_f2(r);
+// cp.async (LDGSTS) helpers: 8-byte global -> shared copies in commit groups.
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
 }
-__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
-  unsigned long long r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(as_u64(a)), "l"(as_u64(b)), "l"(as_u64(c)));
-  return as_f2(r);
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
-__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
-  unsigned long long r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(as_u64(a)), "l"(as_u64(b)));
-  return as_f2(r);
+
+// mbarrier + TMA (cp.async.bulk.tensor) helpers.  One elected thread arms the
+// barrier with the expected byte count and issues the tile copy; every thread
+// waits on the phase parity.
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 3-D tile load (x, y, image) of a CUtensorMap into shared memory
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, uint64_t* bar, int x, int y,
+                                            int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_addr(smem_dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(smem_addr(bar))
+      : "memory");
 }
 
 // image.hpp:34-40 mirror_index: half-sample symmetric reflection, period 2n.
@@ -57,20 +108,22 @@ __host__ __device__ __forceinline__ int mirror_index(int i, int n) {
 // (cos, sin) of 2*pi*p/2^32.  Quadrant from the top bits (after a 1/8-turn
 // offset), residual |r| <= pi/4, paired Horner for sin(r)/r and cos(r).
 // Coefficients: weighted minimax on z = r^2 in [0, (pi/4)^2]; max abs error
-// 6.5e-8 in fp32 (scratch fit).
+// 6.5e-8 in fp32.
 __device__ __forceinline__ void sincos_turns(uint32_t p, float& c_out, float& s_out) {
   const uint32_t pq = p + 0x20000000u;
   const uint32_t q = pq >> 30;
   const int32_t ri = static_cast<int32_t>(pq & 0x3FFFFFFFu) - 0x20000000;
   const float r = static_cast<float>(ri) * 1.4629180792671596e-09f;  // 2 pi / 2^32
   const float z = r * r;
-  const f2 zz{z, z};
-  f2 t{2.716014023462776e-06f, 2.4390450562350452e-05f};
-  t = fma2(t, zz, f2{-1.9839043670799583e-04f, -1.3886763481423259e-03f});
-  t = fma2(t, zz, f2{8.333328180015087e-03f, 4.166662320494652e-02f});
-  t = fma2(t, zz, f2{-1.666666716337204e-01f, -0.5f});
-  t = fma2(t, zz, f2{1.0f, 1.0f});
-  const float sr = r * t.x, cr = t.y;
+  const p2 zz = pk(z, z);
+  p2 t = pk(2.716014023462776e-06f, 2.4390450562350452e-05f);
+  t = fma2(t, zz, pk(-1.9839043670799583e-04f, -1.3886763481423259e-03f));
+  t = fma2(t, zz, pk(8.333328180015087e-03f, 4.166662320494652e-02f));
+  t = fma2(t, zz, pk(-1.666666716337204e-01f, -0.5f));
+  t = fma2(t, zz, pk(1.0f, 1.0f));
+  float ts, tc;
+  upk(t, ts, tc);
+  const float sr = r * ts, cr = tc;
   // rotate by q quarter turns
   const bool odd = q & 1u;
   uint32_t cb = __float_as_uint(odd ? sr : cr);

@@ -8,19 +8,25 @@
 //   work unit = one image, one TW-wide column strip, a run of output rows [y0,y1)
 //   for n = 0..N:
 //     stream input rows y0-W .. y1+W-1 in steps of G rows:
-//       (1) modulate   G x (TW+2W) pixels -> smem M:  (c, f'c, s, f's), c+is = e^{i n w f'}
-//       (2) row pass   G rows x TW outputs (KR per thread, FFMA2)  -> smem ring R
-//                      + the centre (c, s) of each output column     -> smem ring CS
+//       S1  (u, f') rows of this step are in smem (cp.async, issued one step ahead)
+//       (1) modulate   G x (TW+2W) pixels -> smem M: pairs (c, f'c), (s, f's),
+//                      c + i s = e^{i n omega f'} from the exact phase n*u
+//       S2  -> issue cp.async for the next step's (u, f') rows and this step's
+//              running (Q, P) values
+//       (2) row pass   G rows x TW outputs (KR per thread, FFMA2) -> smem ring R
+//                      + the centre (c, s) of each input row      -> smem ring CS
+//       S3
 //       (3) column pass G output rows (KC per thread, FFMA2) from the ring,
-//           demodulate and accumulate (Q, P) of this harmonic into a
-//           workspace that stays L2-resident across n; at n = N divide.
+//           demodulate, accumulate (Q, P) of this harmonic; at n = N divide.
 //
 // Every input row is row-passed once per harmonic (no vertical-halo recompute
-// except 2W rows per work unit), each halo pixel is modulated once, the ring
-// only holds 2W+G rows, and the only HBM traffic besides the (Q,P) workspace
-// is the (u, f') image.  The harmonic phase is the exact uint32 product n*u.
+// except 2W rows per work unit), each halo pixel is modulated once per
+// harmonic, the ring holds 2W+G rows, and global traffic (L2-resident for
+// the most part) is the (u, f') image plus the running (Q, P) per pixel.
 #pragma once
 #include <cuda_runtime.h>
+
+#include <type_traits>
 
 #include "fbf_device.cuh"
 #include "fbf_params.h"
@@ -31,165 +37,250 @@ template <int W_, int TW_, int G_, int KR_, int KC_, int NT_>
 struct FusedCfg {
   static constexpr int W = W_, TW = TW_, G = G_, KR = KR_, KC = KC_, NT = NT_;
   static constexpr int MW = TW + 2 * W;   // modulated row width
-  static constexpr int MP = MW | 1;       // M pitch in float4 (odd: conflict-free column walks)
-  static constexpr int RING = 2 * W + G;  // ring rows
-  static constexpr int RP = TW + 1;       // R pitch in float4
-  static constexpr int CP = TW + 1;       // CS pitch in float2
-  static constexpr size_t smem_bytes =
-      size_t(G) * MP * 16 + size_t(RING) * RP * 16 + size_t(RING) * CP * 8;
+  static constexpr int MP = MW | 1;       // M pitch in 16-byte units (odd: conflict-free column walks)
+  static constexpr int RING = 2 * W + G;  // R ring rows
+  static constexpr int CRING = W + G;     // CS ring rows
+  static constexpr int RP = TW + 1;       // R pitch in 16-byte units
+  static constexpr int CP = TW + 1;       // CS pitch in 8-byte units
+  static constexpr int PROLOGUE = (2 * W + G - 1) / G;  // steps that only row-pass
+  // smem carve-up (bytes; TMA destinations 128-byte aligned)
+  static constexpr size_t up128(size_t v) { return (v + 127) & ~size_t(127); }
+  static constexpr size_t OFF_STAGE = 0;
+  static constexpr size_t OFF_PQ = up128(OFF_STAGE + size_t(G) * MW * 8);
+  static constexpr size_t OFF_M = up128(OFF_PQ + size_t(G) * TW * 8);
+  static constexpr size_t OFF_R = OFF_M + size_t(G) * MP * 16;
+  static constexpr size_t OFF_CS = OFF_R + size_t(RING) * RP * 16;
+  static constexpr size_t OFF_BAR = up128(OFF_CS + size_t(CRING) * CP * 8);
+  static constexpr size_t smem_bytes = OFF_BAR + 16;
   static_assert(G * (TW / KR) == NT, "row pass: one (row, chunk) item per thread");
   static_assert((G / KC) * TW == NT, "column pass: one (column, run) item per thread");
   static_assert(TW % KR == 0 && G % KC == 0, "tiling");
+  static_assert(smem_bytes <= 227 * 1024, "shared memory budget");
+};
+
+// Geometry of one work unit and the rows of step s (same for every harmonic).
+struct Unit {
+  int b, x0, y0, y1;
 };
 
 template <class C>
-__device__ __forceinline__ void modulate_rows(const FusedArgs& A, float4* __restrict__ M, int b,
-                                              int x0, int a, int rows, uint32_t n) {
-  const int tid = threadIdx.x;
-  const int2* __restrict__ uf = A.uf + b * A.g.src_bstride;
-  const int total = rows * C::MW;
-  constexpr int ITER = (C::G * C::MW + C::NT - 1) / C::NT;
-#pragma unroll
-  for (int k = 0; k < ITER; ++k) {
-    const int e = tid + k * C::NT;
-    if (e < total) {
-      const int g = e / C::MW;
-      const int j = e - g * C::MW;
-      const int gy = mirror_index(a + g, A.g.full_height) - A.g.src_row0;
-      const int gx = mirror_index(x0 - C::W + j, A.g.width);
-      const int2 v = __ldg(uf + static_cast<long long>(gy) * A.g.src_pitch + gx);
-      float c, s;
-      sincos_turns(n * static_cast<uint32_t>(v.x), c, s);
-      const float fp = __int_as_float(v.y);
-      M[g * C::MP + j] = make_float4(c, c * fp, s, s * fp);
-    }
+__device__ __forceinline__ void step_rows(const Unit& u, int s, int& a, int& rows, int& o) {
+  if (s < C::PROLOGUE) {  // input rows [y0 - W, y0 + W)
+    a = u.y0 - C::W + s * C::G;
+    rows = min(C::G, u.y0 + C::W - a);
+    o = -1;
+  } else {
+    o = u.y0 + (s - C::PROLOGUE) * C::G;
+    a = o + C::W;
+    rows = min(C::G, u.y1 + C::W - a);
   }
 }
 
+// Warp-row mapping shared by the prefetch and the modulation: warp w owns the
+// step rows g = w, w + NWARP, ...; lane l owns the columns j = l + 32 i of a
+// row.  The mirrored global column of each owned j is computed once per work
+// unit (colofs), so the per-element cost is an add and the copy itself.
 template <class C>
-__device__ __forceinline__ void row_pass(const FusedArgs& A, const float4* __restrict__ M,
-                                         float4* __restrict__ R, f2* __restrict__ CS, int a,
-                                         int rows, int base) {
-  const int tid = threadIdx.x;
-  const int g = tid % C::G;
-  const int xc = (tid / C::G) * C::KR;
-  if (g >= rows) return;
-  const float4* __restrict__ src = M + g * C::MP + xc;
-  const int slot = (a + g - base) % C::RING;
-  f2 accA[C::KR], accB[C::KR];
+struct Lanes {
+  static constexpr int NWARP = C::NT / 32;
+  static constexpr int RPW = C::G / NWARP;      // rows per warp per step
+  static constexpr int NJ = (C::MW + 31) / 32;  // column slots per lane
+  static_assert(C::G % NWARP == 0, "rows per warp");
+};
+
+// TMA loads of one step: the padded (u, f') rows [a, a+G) x columns
+// [x0-W, x0+TW+W) into stage, and the running (Q, P) of output rows [o, o+G)
+// into pqs.  Issued by thread 0 only; rows past the image are zero-filled
+// and never consumed.
+template <class C>
+__device__ __forceinline__ void tma_uf(const FusedArgs& A, int2* stage, uint64_t* bar, const Unit& u,
+                                       int a) {
+  mbar_expect_tx(bar, static_cast<unsigned>(C::G * C::MW * 8));
+  tma_load_3d(stage, &A.tm_uf, bar, u.x0, a - A.g.out_row0 + C::W, u.b);
+}
+template <class C>
+__device__ __forceinline__ void tma_pq(const FusedArgs& A, p2* pqs, uint64_t* bar, const Unit& u, int o) {
+  mbar_expect_tx(bar, static_cast<unsigned>(C::G * C::TW * 8));
+  tma_load_3d(pqs, &A.tm_pq, bar, u.x0, o - A.g.out_row0, u.b);
+}
+
+// Modulation of one step, sliced into RPW*NJ independent elements per thread.
+// Straight-line code: every slot is computed (clamped reads) and only the
+// stores are predicated, so the element chains interleave freely with other
+// work in the same basic block (rows past the step's end hold finite stale
+// data and are never consumed).
+template <class C>
+struct ModNext {
+  static constexpr int ELEMS = Lanes<C>::RPW * Lanes<C>::NJ;
+  const int2* stage;
+  ulonglong2* M;
+  uint32_t n;
+
+  // k must be a constant after unrolling (all callers sit in unrolled loops)
+  __device__ __forceinline__ void element(int k) const {
+    using L = Lanes<C>;
+    const int r = k / L::NJ, i = k % L::NJ;
+    const bool full = (C::MW % 32 == 0) || (i + 1 < L::NJ);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = warp + r * L::NWARP;
+    const int j = lane + 32 * i;
+    const int jc = full ? j : min(j, C::MW - 1);
+    const int2 v = stage[g * C::MW + jc];
+    float c, s;
+    sincos_turns(n * static_cast<uint32_t>(v.x), c, s);
+    const float fp = __int_as_float(v.y);
+    const ulonglong2 m = make_ulonglong2(pk(c, c * fp), pk(s, s * fp));
+    if (full || j < C::MW) M[g * C::MP + j] = m;
+  }
+};
+
+template <class C>
+__device__ __forceinline__ void modulate_rows(const int2* __restrict__ stage, ulonglong2* __restrict__ M,
+                                              int rows, uint32_t n) {
+  (void)rows;
+  const ModNext<C> job{stage, M, n};
 #pragma unroll
-  for (int i = 0; i < C::KR; ++i) accA[i] = accB[i] = f2{0.f, 0.f};
+  for (int k = 0; k < ModNext<C>::ELEMS; ++k) job.element(k);
+}
+
+template <class C>
+__device__ __forceinline__ void row_pass(const FusedArgs& A, const ulonglong2* __restrict__ M,
+                                         ulonglong2* __restrict__ R, p2* __restrict__ CS, int a,
+                                         int rows, int base) {
+  const int g = threadIdx.x % C::G;
+  const int xc = (threadIdx.x / C::G) * C::KR;
+  if (g >= rows) return;
+  const ulonglong2* __restrict__ src = M + g * C::MP + xc;
+  const int rel = a + g - base;
+  const int slot = rel % C::RING;
+  const int cslot = rel % C::CRING;
+  p2 accA[C::KR], accB[C::KR];
+#pragma unroll
+  for (int i = 0; i < C::KR; ++i) accA[i] = accB[i] = 0ull;
 #pragma unroll
   for (int m = 0; m < C::KR + 2 * C::W; ++m) {
-    const float4 v = src[m];
-    const f2 va{v.x, v.y}, vb{v.z, v.w};
+    const ulonglong2 v = src[m];
 #pragma unroll
     for (int i = 0; i < C::KR; ++i) {
       const int j = m - i;
       if (j >= 0 && j <= 2 * C::W) {
-        const int tj = j < C::W ? C::W - j : j - C::W;
-        const float tv = A.k.t[tj];
-        const f2 t{tv, tv};
-        ffma2(accA[i], t, va);
-        ffma2(accB[i], t, vb);
+        const float tv = A.k.t[j < C::W ? C::W - j : j - C::W];
+        accA[i] = fma2(pk(tv, tv), v.x, accA[i]);
+        accB[i] = fma2(pk(tv, tv), v.y, accB[i]);
       }
     }
-    if (m >= C::W && m < C::W + C::KR) CS[slot * C::CP + xc + (m - C::W)] = f2{v.x, v.z};
+    if (m >= C::W && m < C::W + C::KR)  // centre (c, s) of output column xc + m - W
+      CS[cslot * C::CP + xc + (m - C::W)] = pk(lo_of(v.x), lo_of(v.y));
   }
-  float4* __restrict__ dst = R + slot * C::RP + xc;
+  ulonglong2* __restrict__ dst = R + slot * C::RP + xc;
 #pragma unroll
-  for (int i = 0; i < C::KR; ++i) dst[i] = make_float4(accA[i].x, accA[i].y, accB[i].x, accB[i].y);
+  for (int i = 0; i < C::KR; ++i) dst[i] = make_ulonglong2(accA[i], accB[i]);
 }
 
 template <class C>
-__device__ __forceinline__ void col_pass(const FusedArgs& A, const float4* __restrict__ R,
-                                         const f2* __restrict__ CS, int b, int x0, int o, int y1,
-                                         int base, int n) {
-  const int tid = threadIdx.x;
-  const int x = tid % C::TW;
-  const int r0 = o + (tid / C::TW) * C::KC;  // first output row of this thread
-  if (r0 >= y1) return;
-  const int gx = x0 + x;
-  const bool xin = gx < A.g.width;
-  const int nr = min(C::KC, y1 - r0);
-  Pair* __restrict__ pq = A.pq + b * static_cast<long long>(A.g.out_rows) * A.g.width;
-  // prefetch the running (Q, P) of this thread's outputs; latency hides under the FIR
-  Pair prev[C::KC];
-  if (n > 0 && xin) {
+__device__ __forceinline__ void col_pass(const FusedArgs& A, const ulonglong2* __restrict__ R,
+                                         const p2* __restrict__ CS, const p2* __restrict__ pqs,
+                                         const Unit& u, int o, int base, int n, const ModNext<C>& next) {
+  const int x = threadIdx.x % C::TW;
+  const int gi = (threadIdx.x / C::TW) * C::KC;  // first output row of this thread, rel. to o
+  const int r0 = o + gi;
+  const int gx = u.x0 + x;
+  const int nr = min(C::KC, u.y1 - r0);  // <= 0: this thread only helps with the modulation
+  p2 accA[C::KC], accB[C::KC];
 #pragma unroll
-    for (int i = 0; i < C::KC; ++i)
-      if (i < nr) {
-        const long long idx = static_cast<long long>(r0 + i - A.g.out_row0) * A.g.width + gx;
-        prev[i] = pq[idx];
-      }
-  }
-  f2 accA[C::KC], accB[C::KC];
-#pragma unroll
-  for (int i = 0; i < C::KC; ++i) accA[i] = accB[i] = f2{0.f, 0.f};
+  for (int i = 0; i < C::KC; ++i) accA[i] = accB[i] = 0ull;
   const int s0 = (r0 - C::W - base) % C::RING;
+  constexpr int TAPS_IN = C::KC + 2 * C::W;
+  constexpr int ELEMS = ModNext<C>::ELEMS;
+  constexpr int STRIDE = TAPS_IN / ELEMS > 0 ? TAPS_IN / ELEMS : 1;
 #pragma unroll
-  for (int m = 0; m < C::KC + 2 * C::W; ++m) {
+  for (int m = 0; m < TAPS_IN; ++m) {
     int s = s0 + m;
     s = s >= C::RING ? s - C::RING : s;
-    s = s >= C::RING ? s - C::RING : s;
-    const float4 v = R[s * C::RP + x];
-    const f2 va{v.x, v.y}, vb{v.z, v.w};
+    const ulonglong2 v = R[s * C::RP + x];
 #pragma unroll
     for (int i = 0; i < C::KC; ++i) {
       const int j = m - i;
       if (j >= 0 && j <= 2 * C::W) {
-        const int tj = j < C::W ? C::W - j : j - C::W;
-        const float tv = A.k.t[tj];
-        const f2 t{tv, tv};
-        ffma2(accA[i], t, va);
-        ffma2(accB[i], t, vb);
+        const float tv = A.k.t[j < C::W ? C::W - j : j - C::W];
+        accA[i] = fma2(pk(tv, tv), v.x, accA[i]);
+        accB[i] = fma2(pk(tv, tv), v.y, accB[i]);
       }
     }
+    // one slice of the next step's modulation per STRIDE taps
+    if (m % STRIDE == 0 && m / STRIDE < ELEMS) next.element(m / STRIDE);
   }
-  if (!xin) return;
+#pragma unroll
+  for (int k = TAPS_IN / STRIDE + (TAPS_IN % STRIDE ? 1 : 0); k < ELEMS; ++k) next.element(k);
+  if (nr <= 0 || gx >= A.g.width) return;
   const float dn = A.h.d[n];
+  const p2 dd = pk(dn, dn);
   const bool last = (n == A.h.N);
+  const int cs0 = (r0 - base) % C::CRING;
+  p2* __restrict__ pqrow = reinterpret_cast<p2*>(A.pq) +
+                           (u.b * static_cast<long long>(A.g.out_rows) + (r0 - A.g.out_row0)) * A.pq_cols + gx;
+  const int wstride = A.pq_cols;
+  // demodulate all KC outputs straight-line; only the global stores are predicated
+  p2 qp[C::KC];
 #pragma unroll
   for (int i = 0; i < C::KC; ++i) {
-    if (i >= nr) break;
-    const int y = r0 + i;
-    int sc = s0 + C::W + i;
-    sc = sc >= C::RING ? sc - C::RING : sc;
-    sc = sc >= C::RING ? sc - C::RING : sc;
-    const f2 cs = CS[sc * C::CP + x];
-    // (q, p) = c*(Gc, Fc) + s*(Gs, Fs)   [bilateral.hpp:138-144, real form]
-    f2 qp = mul2(f2{cs.x, cs.x}, accA[i]);
-    qp = fma2(f2{cs.y, cs.y}, accB[i], qp);
-    f2 acc;
+    int sc = cs0 + i;
+    sc = sc >= C::CRING ? sc - C::CRING : sc;
+    float c, s;
+    upk(CS[sc * C::CP + x], c, s);
+    // (q, p) = c (Gc, Fc) + s (Gs, Fs)   [bilateral.hpp:138-144, real form]
+    qp[i] = fma2(pk(s, s), accB[i], mul2(pk(c, c), accA[i]));
+  }
+  if (!last) {
     if (n == 0) {
-      acc = mul2(f2{dn, dn}, qp);
+#pragma unroll
+      for (int i = 0; i < C::KC; ++i)
+        if (i < nr) pqrow[i * wstride] = mul2(dd, qp[i]);
     } else {
-      acc = fma2(f2{dn, dn}, qp, f2{prev[i].x, prev[i].y});
+#pragma unroll
+      for (int i = 0; i < C::KC; ++i)
+        if (i < nr) pqrow[i * wstride] = fma2(dd, qp[i], pqs[(gi + i) * C::TW + x]);
     }
-    const long long idx = static_cast<long long>(y - A.g.out_row0) * A.g.width + gx;
-    if (!last) {
-      pq[idx] = Pair{acc.x, acc.y};
-    } else {
-      // bilateral.hpp:147-158: divide; flag the first collapsed denominator
-      const float Q = acc.x, P = acc.y;
-      if (!(fabsf(Q) >= A.h.q_floor)) {
+    return;
+  }
+  // bilateral.hpp:147-158: divide; flag the first collapsed denominator
+  float* __restrict__ drow = A.dst + u.b * A.g.dst_bstride +
+                             static_cast<long long>(r0 - A.g.out_row0) * A.g.dst_pitch + gx;
+#pragma unroll
+  for (int i = 0; i < C::KC; ++i) {
+    if (i < nr) {
+      const p2 acc = (n == 0) ? mul2(dd, qp[i]) : fma2(dd, qp[i], pqs[(gi + i) * C::TW + x]);
+      float Q, P;
+      upk(acc, Q, P);
+      if (!(fabsf(Q) >= A.h.q_floor) && A.bad) {
         const unsigned long long lin =
-            static_cast<unsigned long long>(b) * A.g.full_height * A.g.width +
-            static_cast<unsigned long long>(y) * A.g.width + gx;
+            static_cast<unsigned long long>(u.b) * A.g.full_height * A.g.width +
+            static_cast<unsigned long long>(r0 + i) * A.g.width + gx;
         atomicMin(A.bad, lin);
       }
-      A.dst[b * A.g.dst_bstride + static_cast<long long>(y - A.g.out_row0) * A.g.dst_pitch + gx] =
-          A.h.shift + __fdiv_rn(P, Q);
+      drow[i * static_cast<long long>(A.g.dst_pitch)] = A.h.shift + __fdiv_rn(P, Q);
     }
   }
 }
 
 template <class C>
-__global__ void __launch_bounds__(C::NT, 1) fused_kernel(const __grid_constant__ FusedArgs A) {
-  extern __shared__ float4 smem[];
-  float4* M = smem;
-  float4* R = M + C::G * C::MP;
-  f2* CS = reinterpret_cast<f2*>(R + C::RING * C::RP);
+__global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(const __grid_constant__ FusedArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int2* stage = reinterpret_cast<int2*>(smem + C::OFF_STAGE);
+  ulonglong2* M = reinterpret_cast<ulonglong2*>(smem + C::OFF_M);
+  ulonglong2* R = reinterpret_cast<ulonglong2*>(smem + C::OFF_R);
+  p2* CS = reinterpret_cast<p2*>(smem + C::OFF_CS);
+  p2* pqs = reinterpret_cast<p2*>(smem + C::OFF_PQ);
+  uint64_t* bar_uf = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* bar_pq = bar_uf + 1;
+  const bool leader = threadIdx.x == 0;
+  if (leader) {
+    mbar_init(bar_uf, 1);
+    mbar_init(bar_pq, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  unsigned ph_uf = 0, ph_pq = 0;  // phase parity of the next completion of each barrier
 
   const long long total = A.total;
   const long long lo = total * blockIdx.x / gridDim.x;
@@ -199,52 +290,114 @@ __global__ void __launch_bounds__(C::NT, 1) fused_kernel(const __grid_constant__
     const int r0 = static_cast<int>(pos - sidx * A.g.out_rows);
     const int len = static_cast<int>(min(min(static_cast<long long>(A.g.out_rows - r0), hi - pos),
                                          static_cast<long long>(A.seg_max)));
-    const int b = static_cast<int>(sidx / A.strips);
-    const int x0 = static_cast<int>(sidx - static_cast<long long>(b) * A.strips) * C::TW;
-    const int y0 = A.g.out_row0 + r0, y1 = y0 + len;
-    const int base = y0 - C::W;
+    Unit u;
+    u.b = static_cast<int>(sidx / A.strips);
+    u.x0 = static_cast<int>(sidx - static_cast<long long>(u.b) * A.strips) * C::TW;
+    u.y0 = A.g.out_row0 + r0;
+    u.y1 = u.y0 + len;
+    const int base = u.y0 - C::W;
+    const int nsteps = C::PROLOGUE + (len + C::G - 1) / C::G;
+
+    {  // bootstrap: step 0 of harmonic 0 into M
+      int a, rows, o;
+      step_rows<C>(u, 0, a, rows, o);
+      __syncthreads();  // the previous unit finished reading stage and M
+      if (leader) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tma_uf<C>(A, stage, bar_uf, u, a);
+      }
+      mbar_wait(bar_uf, ph_uf);
+      ph_uf ^= 1u;
+      modulate_rows<C>(stage, M, rows, 0u);
+    }
     for (int n = 0; n <= A.h.N; ++n) {
-      // prologue: the 2W input rows above the first output row
-      for (int a = y0 - C::W; a < y0 + C::W; a += C::G) {
-        const int rows = min(C::G, y0 + C::W - a);
-        modulate_rows<C>(A, M, b, x0, a, rows, static_cast<uint32_t>(n));
-        __syncthreads();
+      for (int s = 0; s < nsteps; ++s) {
+        int a, rows, o, a2, rows2, o2;
+        step_rows<C>(u, s, a, rows, o);
+        const bool wrap = s + 1 == nsteps;  // next step is step 0 of harmonic n+1
+        const bool more = !wrap || n < A.h.N;
+        const bool want_pq = o >= 0 && n > 0;
+        step_rows<C>(u, wrap ? 0 : s + 1, a2, rows2, o2);
+        __syncthreads();  // S1: M holds this step; the previous column pass is done; stage free
+        if (leader) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (more) tma_uf<C>(A, stage, bar_uf, u, a2);
+          if (want_pq) tma_pq<C>(A, pqs, bar_pq, u, o);
+        }
         row_pass<C>(A, M, R, CS, a, rows, base);
-        __syncthreads();
+        if (more) {
+          mbar_wait(bar_uf, ph_uf);
+          ph_uf ^= 1u;
+        }
+        if (want_pq) {
+          mbar_wait(bar_pq, ph_pq);
+          ph_pq ^= 1u;
+        }
+        __syncthreads();  // S2: ring rows visible, next (u, f') and this step's (Q, P) landed, M free
+        // the next step's modulation is interleaved into this step's column pass
+        // (its ALU work issues in the FFMA2 shadow); prologue steps run it alone
+        const ModNext<C> next{stage, M, static_cast<uint32_t>(wrap ? n + 1 : n)};
+        if (o >= 0)
+          col_pass<C>(A, R, CS, pqs, u, o, base, n, next);
+        else
+          modulate_rows<C>(stage, M, rows2, next.n);
       }
-      for (int o = y0; o < y1; o += C::G) {
-        const int a = o + C::W;
-        const int rows = min(C::G, y1 + C::W - a);
-        modulate_rows<C>(A, M, b, x0, a, rows, static_cast<uint32_t>(n));
-        __syncthreads();
-        row_pass<C>(A, M, R, CS, a, rows, base);
-        __syncthreads();
-        col_pass<C>(A, R, CS, b, x0, o, y1, base, n);
-      }
-      __syncthreads();
     }
     pos += len;
   }
 }
 
-// Per-radius launch configuration (TW=64 columns per strip, G=32 rows per step,
-// 8 outputs per thread in both passes, 256 threads).
+// Launch configuration per radius: TW=64 columns per strip, 8 outputs per
+// thread in both passes.  W <= 15: G=16 rows per step, 128 threads, ~108 KB
+// of smem -> two independent CTAs per SM (their barriers interleave).
+// Larger W: the 2W+G ring needs G=32 / 256 threads / one CTA per SM.
 template <int W>
-using Cfg = FusedCfg<W, 64, 32, 8, 8, 256>;
+using Cfg = typename std::conditional<(W <= 15), FusedCfg<W, 64, 16, 8, 8, 128>,
+                                      FusedCfg<W, 64, 32, 8, 8, 256>>::type;
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+inline cudaError_t encode_tile_3d(CUtensorMap* m, const void* base, unsigned long long d0,
+                                  unsigned long long d1, unsigned long long d2, unsigned b0, unsigned b1) {
+  using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                          const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                          CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Fn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !p) return cudaErrorNotSupported;
+    fn = reinterpret_cast<Fn>(p);
+  }
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {d0 * 8, d0 * d1 * 8};
+  const cuuint32_t box[3] = {b0, b1, 1};
+  const cuuint32_t estride[3] = {1, 1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, const_cast<void*>(base), dims, strides, box,
+                        estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
 
 template <int W>
 cudaError_t launch_w(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
   using C = Cfg<W>;
+  static_assert(C::TW == kFusedTW, "workspace layout assumes kFusedTW-wide strips");
   FusedArgs a = a_in;
   a.strips = (a.g.width + C::TW - 1) / C::TW;
+  a.pq_cols = a.strips * C::TW;
   a.total = static_cast<long long>(a.g.batch) * a.strips * a.g.out_rows;
-  static bool configured = false;  // benign race: idempotent attribute set
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(fused_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(C::smem_bytes));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = encode_tile_3d(&a.tm_uf, a.uf, static_cast<unsigned long long>(a.pq_cols + 2 * W),
+                                 static_cast<unsigned long long>(a.g.out_rows + 2 * W),
+                                 static_cast<unsigned long long>(a.g.batch), C::MW, C::G);
+  if (e != cudaSuccess) return e;
+  e = encode_tile_3d(&a.tm_pq, a.pq, static_cast<unsigned long long>(a.pq_cols),
+                     static_cast<unsigned long long>(a.g.out_rows), static_cast<unsigned long long>(a.g.batch),
+                     C::TW, C::G);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fused_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(C::smem_bytes));
+  if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -1,11 +1,14 @@
 // fbf_params.h -- launch parameter blocks (passed by value: they live in the
 // kernel's constant bank, so taps and coefficients are uniform operands).
 #pragma once
+#include <cuda.h>  // CUtensorMap (type only; encoded through the runtime's driver entry point)
+
 #include <cstdint>
 
 namespace fbf {
 
 constexpr int kMaxN = 127;  // highest harmonic supported by one launch
+constexpr int kFusedTW = 64;  // column-strip width of the fused kernel (workspace layout)
 constexpr int kMaxW = 64;   // largest spatial radius supported by the fused/naive paths
 
 struct Pair {
@@ -43,7 +46,14 @@ struct Taps {
   float t[kMaxW + 1];     // tap |j| (spatial.hpp profile[W+j]); broadcast to both FFMA2 lanes
 };
 
+// Fused path: the prep kernel writes a mirror-PADDED (u, f') image per image,
+// rows = out_rows + 2W (global rows out_row0-W ...), columns = strips*TW + 2W
+// (global columns -W ...), so every step's tile is an in-bounds TMA box; the
+// running (Q, P) workspace is out_rows x strips*TW per image.
 struct FusedArgs {
+  CUtensorMap tm_uf;  // int64 elements (u, f'), dims {uf_cols, out_rows + 2W, batch}, box {TW+2W, G, 1}
+  CUtensorMap tm_pq;  // int64 elements (Q, P),  dims {pq_cols, out_rows, batch},     box {TW, G, 1}
+  int pq_cols;        // strips * TW
   Geometry g;
   Harmonics h;
   Taps k;
