@@ -56,17 +56,6 @@ def dist_env():
     return ws, rank, local
 
 
-def shard(cfg, world, rank):
-    """(image indices, out_row0, out_rows) owned by `rank`."""
-    if cfg.batch > 1:
-        b0 = cfg.batch * rank // world
-        b1 = cfg.batch * (rank + 1) // world
-        return list(range(b0, b1)), 0, cfg.height
-    r0 = cfg.height * rank // world
-    r1 = cfg.height * (rank + 1) // world
-    return [0], r0, r1 - r0
-
-
 class ClockSampler:
     """nvidia-smi-equivalent sampling (NVML) of SM clock + throttle reasons during the timed region."""
 
@@ -201,6 +190,8 @@ def main():
     import torch.distributed as dist
     import paper_1603_08081_b200 as fb
     from paper_1603_08081_b200.configs import approx_of, image_of, spatial_of
+    from paper_1603_08081_b200.shard import geometry as shard_geometry
+    from paper_1603_08081_b200.shard import plan
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -211,13 +202,12 @@ def main():
 
     spatial, approx = spatial_of(cfg), approx_of(cfg)
     W = spatial.radius
-    images, out_row0, out_rows = shard(cfg, world, rank)
+    part = plan(cfg.width, cfg.height, cfg.batch, W, world, rank)
+    geo = shard_geometry(part, cfg.width, cfg.height)
     if cfg.batch > 1:
-        geo = fb.whole_geometry(cfg.width, cfg.height, len(images))
-        host = np.stack([image_of(cfg, i) for i in images])
-    else:
-        geo = fb.strip_geometry(cfg.width, cfg.height, out_row0, out_rows, W)
-        host = image_of(cfg, 0, geo.src_row0, geo.src_rows)[None]
+        host = np.stack([image_of(cfg, i) for i in part.images])
+    else:  # each rank generates only its own strip (with halo rows)
+        host = image_of(cfg, 0, part.src_row0, part.src_rows)[None]
     nb = host.shape[0]
     src = torch.from_numpy(host).to(dev)
     dst = torch.empty((nb, geo.out_rows, cfg.width), dtype=torch.float32, device=dev)

@@ -577,6 +577,8 @@ int fbf_bilateral_fast_host_f64(const fbf_geometry* g, const fbf_filter* f, cons
                                 double* dst, int variant, long long* bad_index) {
   int rc = check_geometry(g);
   if (rc) return rc;
+  if ((rc = check_filter(f))) return rc;  // validate before touching the device
+  if ((rc = check_halo(g, f->radius))) return rc;
   fbf_geometry gd = *g;
   gd.src_pitch = g->width;
   gd.dst_pitch = g->width;

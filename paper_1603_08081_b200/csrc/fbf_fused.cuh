@@ -26,6 +26,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "fbf_device.cuh"
@@ -379,9 +380,9 @@ inline cudaError_t encode_tile_3d(CUtensorMap* m, const void* base, unsigned lon
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <int W>
-cudaError_t launch_w(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
-  using C = Cfg<W>;
+template <class C>
+cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
+  constexpr int W = C::W;
   static_assert(C::TW == kFusedTW, "workspace layout assumes kFusedTW-wide strips");
   FusedArgs a = a_in;
   a.strips = (a.g.width + C::TW - 1) / C::TW;
@@ -412,6 +413,20 @@ cudaError_t launch_w(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
   if (grid_out) *grid_out = static_cast<int>(grid);
   fused_kernel<C><<<static_cast<unsigned>(grid), C::NT, C::smem_bytes, st>>>(a);
   return cudaGetLastError();
+}
+
+// Experiment switch (FBF_FUSED_CFG=small|big) for radii where both fit.
+template <int W>
+cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
+  using Small = FusedCfg<W, 64, 16, 8, 8, 128>;
+  using Big = FusedCfg<W, 64, 32, 8, 8, 256>;
+  if constexpr (Small::smem_bytes <= 113 * 1024) {
+    const char* env = getenv("FBF_FUSED_CFG");
+    // measured (profiles/r01_cfg_compare.txt): small wins only for W <= 9
+    const bool big = env ? env[0] == 'b' : !(W <= 9);
+    if (!big) return launch_cfg<Small>(a, st, grid_out);
+  }
+  return launch_cfg<Big>(a, st, grid_out);
 }
 
 }  // namespace fbf

@@ -1,0 +1,65 @@
+"""GPU: the device-resident C-ABI path (fbf_prepare_device + fbf_filter_prepared_device
+on torch-allocated HBM buffers), as bench.py and the multi-GPU driver use it.
+
+* row strips with W halo rows (the multi-GPU shard plan, emulated rank by rank
+  on one GPU -- no rank waits on another) reassemble to the whole-image result
+  bit for bit, at full BASELINE sizes (a size-independent property);
+* the harmonic range is a pure function of the inputs (bit-identical reruns).
+"""
+import numpy as np
+import pytest
+
+import paper_1603_08081_b200 as fb
+from paper_1603_08081_b200.configs import CONFIGS, approx_of, image_of, spatial_of
+from paper_1603_08081_b200.shard import geometry, plan
+
+pytestmark = pytest.mark.gpu
+
+
+def run_device(img_rows, geo, s, a, variant="fused", check_eps=True):
+    import torch
+    dev = torch.device("cuda", 0)
+    src = torch.from_numpy(np.ascontiguousarray(img_rows, dtype=np.float32)).to(dev)
+    nb = 1 if img_rows.ndim == 2 else img_rows.shape[0]
+    dst = torch.empty((nb, geo.out_rows, geo.width), dtype=torch.float32, device=dev)
+    ws_bytes = fb.workspace_bytes(geo, s.radius, variant)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    bad = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    fb.prepare_device(src.data_ptr(), geo, s, a, ws.data_ptr(), ws_bytes, st, variant, check_eps)
+    fb.filter_prepared_device(dst.data_ptr(), geo, s, a, ws.data_ptr(), ws_bytes, bad.data_ptr(), st, variant,
+                              check_eps)
+    torch.cuda.synchronize()
+    assert int(bad.item()) == -1
+    return dst.cpu().numpy()
+
+
+@pytest.mark.parametrize("name,world", [("c2", 8), ("c4", 8), ("c1", 3), ("c3", 5)])
+def test_row_strips_reassemble_bit_identically(name, world):
+    c = CONFIGS[name]
+    img, s, a = image_of(c), spatial_of(c), approx_of(c)
+    whole = run_device(img, fb.whole_geometry(c.width, c.height), s, a, check_eps=c.check_epsilon)[0]
+    parts = []
+    for r in range(world):
+        sh = plan(c.width, c.height, 1, s.radius, world, r)
+        parts.append(run_device(img[sh.src_row0:sh.src_row0 + sh.src_rows], geometry(sh, c.width, c.height),
+                                s, a, check_eps=c.check_epsilon)[0])
+    assert np.array_equal(np.concatenate(parts), whole)
+
+
+def test_batch_shards_match_whole_batch():
+    c = CONFIGS["c5"]
+    s, a = spatial_of(c), approx_of(c)
+    imgs = np.stack([image_of(c, i) for i in range(8)])
+    whole = run_device(imgs, fb.whole_geometry(c.width, c.height, 8), s, a)
+    for r in range(4):
+        sh = plan(c.width, c.height, 8, s.radius, 4, r)
+        part = run_device(imgs[sh.images], geometry(sh, c.width, c.height), s, a)
+        assert np.array_equal(part, whole[sh.images])
+
+
+def test_device_path_matches_host_path():
+    c = CONFIGS["c1"]
+    img, s, a = image_of(c), spatial_of(c), approx_of(c)
+    dev = run_device(img, fb.whole_geometry(c.width, c.height), s, a)[0]
+    assert np.array_equal(dev, fb.bilateral_fast(img, s, a))
