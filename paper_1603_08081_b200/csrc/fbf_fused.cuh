@@ -26,7 +26,6 @@
 #pragma once
 #include <cuda_runtime.h>
 
-#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -119,11 +118,7 @@ struct ModNext {
   uint32_t n;
 
   // k must be a constant after unrolling (all callers sit in unrolled loops)
-  // `zero` is an opaque 0 that callers may derive from a value computed late in
-  // their own loop: it pins the element's stage load (and so its whole chain)
-  // after that point, spreading the modulation across the FFMA2 stream instead
-  // of letting the scheduler hoist all of it to the front.
-  __device__ __forceinline__ void element(int k, int zero = 0) const {
+  __device__ __forceinline__ void element(int k) const {
     using L = Lanes<C>;
     const int r = k / L::NJ, i = k % L::NJ;
     const bool full = (C::MW % 32 == 0) || (i + 1 < L::NJ);
@@ -131,7 +126,7 @@ struct ModNext {
     const int g = warp + r * L::NWARP;
     const int j = lane + 32 * i;
     const int jc = full ? j : min(j, C::MW - 1);
-    const int2 v = stage[g * C::MW + jc + zero];
+    const int2 v = stage[g * C::MW + jc];
     float c, s;
     sincos_turns(n * static_cast<uint32_t>(v.x), c, s);
     const float fp = __int_as_float(v.y);
@@ -186,8 +181,7 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const ulonglong2* _
 template <class C>
 __device__ __forceinline__ void col_pass(const FusedArgs& A, const ulonglong2* __restrict__ R,
                                          const p2* __restrict__ CS, const p2* __restrict__ pqs,
-                                         const Unit& u, int o, int base, int n, uint64_t* bar_pq,
-                                         unsigned ph_pq) {
+                                         const Unit& u, int o, int base, int n, const ModNext<C>& next) {
   const int x = threadIdx.x % C::TW;
   const int gi = (threadIdx.x / C::TW) * C::KC;  // first output row of this thread, rel. to o
   const int r0 = o + gi;
@@ -198,6 +192,8 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const ulonglong2* _
   for (int i = 0; i < C::KC; ++i) accA[i] = accB[i] = 0ull;
   const int s0 = (r0 - C::W - base) % C::RING;
   constexpr int TAPS_IN = C::KC + 2 * C::W;
+  constexpr int ELEMS = ModNext<C>::ELEMS;
+  constexpr int STRIDE = TAPS_IN / ELEMS > 0 ? TAPS_IN / ELEMS : 1;
 #pragma unroll
   for (int m = 0; m < TAPS_IN; ++m) {
     int s = s0 + m;
@@ -212,9 +208,12 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const ulonglong2* _
         accB[i] = fma2(pk(tv, tv), v.y, accB[i]);
       }
     }
+    // one slice of the next step's modulation per STRIDE taps
+    if (m % STRIDE == 0 && m / STRIDE < ELEMS) next.element(m / STRIDE);
   }
+#pragma unroll
+  for (int k = TAPS_IN / STRIDE + (TAPS_IN % STRIDE ? 1 : 0); k < ELEMS; ++k) next.element(k);
   if (nr <= 0 || gx >= A.g.width) return;
-  if (bar_pq) mbar_wait(bar_pq, ph_pq);  // this step's running (Q, P) tile
   const float dn = A.h.d[n];
   const p2 dd = pk(dn, dn);
   const bool last = (n == A.h.N);
@@ -241,7 +240,7 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const ulonglong2* _
     } else {
 #pragma unroll
       for (int i = 0; i < C::KC; ++i)
-        if (i < nr && A.expt < 5) pqrow[i * wstride] = fma2(dd, qp[i], pqs[(gi + i) * C::TW + x]);
+        if (i < nr) pqrow[i * wstride] = fma2(dd, qp[i], pqs[(gi + i) * C::TW + x]);
     }
     return;
   }
@@ -283,7 +282,6 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
   }
   __syncthreads();
   unsigned ph_uf = 0, ph_pq = 0;  // phase parity of the next completion of each barrier
-  long long pacc[12] = {0};       // diagnostics (A.prof): per-phase cycles of this thread
 
   const long long total = A.total;
   const long long lo = total * blockIdx.x / gridDim.x;
@@ -305,17 +303,12 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
       int a, rows, o;
       step_rows<C>(u, 0, a, rows, o);
       __syncthreads();  // the previous unit finished reading stage and M
-      const long long b0 = A.prof ? clock64() : 0;
       if (leader) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tma_uf<C>(A, stage, bar_uf, u, a);
       }
       mbar_wait(bar_uf, ph_uf);
       ph_uf ^= 1u;
-      if (A.prof) {
-        pacc[10] += clock64() - b0;
-        pacc[11] += 1;
-      }
       modulate_rows<C>(stage, M, rows, 0u);
     }
     for (int n = 0; n <= A.h.N; ++n) {
@@ -324,88 +317,36 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
         step_rows<C>(u, s, a, rows, o);
         const bool wrap = s + 1 == nsteps;  // next step is step 0 of harmonic n+1
         const bool more = !wrap || n < A.h.N;
-        const bool want_pq = o >= 0 && n > 0 && A.expt < 4;
+        const bool want_pq = o >= 0 && n > 0;
         step_rows<C>(u, wrap ? 0 : s + 1, a2, rows2, o2);
-        const long long t0 = A.prof ? clock64() : 0;
         __syncthreads();  // S1: M holds this step; the previous column pass is done; stage free
-        const long long t1 = A.prof ? clock64() : 0;
         if (leader) {
-          // no proxy fence: these TMA writes only follow generic-proxy READS of
-          // stage/pqs, ordered by the block barrier (a fence here also waited
-          // for the leader's outstanding (Q, P) stores: +3000 cycles per step)
-          if (A.expt == 3) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           if (more) tma_uf<C>(A, stage, bar_uf, u, a2);
           if (want_pq) tma_pq<C>(A, pqs, bar_pq, u, o);
-          // warm L2 one step further ahead (HBM latency exceeds one row pass):
-          // (u, f') of step s+2 and the running (Q, P) of step s+1
-          int s3 = s + 2, n3 = A.expt == 2 ? A.h.N + 1 : n;
-          if (s3 >= nsteps) { s3 -= nsteps; ++n3; }
-          if (n3 <= A.h.N) {
-            int a3, rows3, o3;
-            step_rows<C>(u, s3, a3, rows3, o3);
-            tma_prefetch_3d(&A.tm_uf, u.x0, a3 - A.g.out_row0 + C::W, u.b);
-          }
-          if (A.expt != 2 && !wrap && o2 >= 0 && n > 0) tma_prefetch_3d(&A.tm_pq, u.x0, o2 - A.g.out_row0, u.b);
-          if (A.expt != 2 && wrap && n < A.h.N) {  // first output step of harmonic n+1
-            int a4, rows4, o4;
-            step_rows<C>(u, C::PROLOGUE, a4, rows4, o4);
-            if (o4 < u.y1) tma_prefetch_3d(&A.tm_pq, u.x0, o4 - A.g.out_row0, u.b);
-          }
-        }
-        if (A.expt && A.prof) {  // diagnostics: TMA latency with the whole CTA idle
-          const long long q0 = clock64();
-          if (more) mbar_wait(bar_uf, ph_uf);
-          const long long q1 = clock64();
-          if (want_pq) mbar_wait(bar_pq, ph_pq);
-          const long long q2 = clock64();
-          __syncthreads();
-          pacc[8] += q1 - q0;
-          pacc[9] += q2 - q1;
         }
         row_pass<C>(A, M, R, CS, a, rows, base);
-        const long long t2 = A.prof ? clock64() : 0;
-        __syncthreads();  // S2: ring rows visible; M free
-        const long long t3 = A.prof ? clock64() : 0;
-        // Column pass.  Its (Q, P) tile is only needed by the demodulation at
-        // the end, so each thread waits on that TMA right there (mbarrier
-        // completion is visible to every waiter; no block barrier needed):
-        // the load gets the whole row pass + column FIR to land.
-        if (o >= 0) col_pass<C>(A, R, CS, pqs, u, o, base, n, want_pq ? bar_pq : nullptr, ph_pq);
-        if (want_pq) ph_pq ^= 1u;
-        const long long t4 = A.prof ? clock64() : 0;
-        // The next step's (u, f') is likewise waited for only now, then
-        // modulated into M for the next row pass.
         if (more) {
           mbar_wait(bar_uf, ph_uf);
           ph_uf ^= 1u;
         }
-        const long long t5 = A.prof ? clock64() : 0;
-        modulate_rows<C>(stage, M, rows2, static_cast<uint32_t>(wrap ? n + 1 : n));
-        if (A.prof) {
-          const long long t6 = clock64();
-          pacc[0] += t1 - t0;  // S1 wait
-          pacc[1] += t2 - t1;  // row pass
-          pacc[2] += t3 - t2;  // S2 wait
-          pacc[3] += t4 - t3;  // column pass (+ (Q, P) wait) + demod
-          pacc[4] += t5 - t4;  // (u, f') wait
-          pacc[5] += t6 - t5;  // modulation
-          pacc[7] += 1;
+        if (want_pq) {
+          mbar_wait(bar_pq, ph_pq);
+          ph_pq ^= 1u;
         }
+        __syncthreads();  // S2: ring rows visible, next (u, f') and this step's (Q, P) landed, M free
+        // the next step's modulation is interleaved into this step's column pass
+        // (its ALU work issues in the FFMA2 shadow); prologue steps run it alone
+        const ModNext<C> next{stage, M, static_cast<uint32_t>(wrap ? n + 1 : n)};
+        if (o >= 0)
+          col_pass<C>(A, R, CS, pqs, u, o, base, n, next);
+        else
+          modulate_rows<C>(stage, M, rows2, next.n);
       }
     }
     pos += len;
   }
-  if (A.prof && (threadIdx.x & 31) == 0)  // one flush per warp: no contention during the run
-    for (int k = 0; k < 12; ++k) atomicAdd(A.prof + k, static_cast<unsigned long long>(pacc[k]));
 }
-
-// Launch configuration per radius: TW=64 columns per strip, 8 outputs per
-// thread in both passes.  W <= 15: G=16 rows per step, 128 threads, ~108 KB
-// of smem -> two independent CTAs per SM (their barriers interleave).
-// Larger W: the 2W+G ring needs G=32 / 256 threads / one CTA per SM.
-template <int W>
-using Cfg = typename std::conditional<(W <= 15), FusedCfg<W, 64, 16, 8, 8, 128>,
-                                      FusedCfg<W, 64, 32, 8, 8, 256>>::type;
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 inline cudaError_t encode_tile_3d(CUtensorMap* m, const void* base, unsigned long long d0,
@@ -462,39 +403,19 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
   if (grid > by_work) grid = by_work;
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = static_cast<int>(grid);
-  const char* prof_env = getenv("FBF_PROF");  // diagnostics: per-phase SM cycles to stderr
-  unsigned long long* prof = nullptr;
-  if (prof_env && prof_env[0] == '1') {
-    cudaMallocAsync(reinterpret_cast<void**>(&prof), 16 * sizeof(unsigned long long), st);
-    cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st);
-    a.prof = prof;
-    const char* ex = getenv("FBF_EXPT");
-    a.expt = ex ? ex[0] - '0' : 0;
-  }
   fused_kernel<C><<<static_cast<unsigned>(grid), C::NT, C::smem_bytes, st>>>(a);
-  if (prof) {
-    unsigned long long h[16];
-    cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    cudaFreeAsync(prof, st);
-    const char* names[7] = {"S1wait", "rowpass", "S2wait", "colpass", "ufwait", "modulate", "-"};
-    const double steps = h[7] ? static_cast<double>(h[7]) : 1.0;
-    fprintf(stderr, "[fbf prof W=%d grid=%lld] warp-steps %.0f:", W, grid, steps);
-    for (int k = 0; k < 6; ++k) fprintf(stderr, " %s %.0f", names[k], h[k] / steps);
-    fprintf(stderr, " | isolated uf-latency %.0f pq-extra %.0f | bootstrap uf %.0f (n=%llu)\n", h[8] / steps,
-            h[9] / steps, h[11] ? static_cast<double>(h[10]) / h[11] : 0.0, h[11]);
-  }
   return cudaGetLastError();
 }
 
-// Experiment switch (FBF_FUSED_CFG=small|big) for radii where both fit.
+// Small (128 threads, G=16, two CTAs per SM) for W <= 9, big (256 threads,
+// G=32, one CTA per SM) otherwise -- measured, profiles/r01_cfg_compare.txt.
+// FBF_FUSED_CFG=small|big overrides where both fit (experiments).
 template <int W>
 cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
   using Small = FusedCfg<W, 64, 16, 8, 8, 128>;
   using Big = FusedCfg<W, 64, 32, 8, 8, 256>;
   if constexpr (Small::smem_bytes <= 113 * 1024) {
     const char* env = getenv("FBF_FUSED_CFG");
-    // measured (profiles/r01_cfg_compare.txt): small wins only for W <= 9
     const bool big = env ? env[0] == 'b' : !(W <= 9);
     if (!big) return launch_cfg<Small>(a, st, grid_out);
   }

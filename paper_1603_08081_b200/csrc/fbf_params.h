@@ -54,8 +54,6 @@ struct FusedArgs {
   CUtensorMap tm_uf;  // int64 elements (u, f'), dims {uf_cols, out_rows + 2W, batch}, box {TW+2W, G, 1}
   CUtensorMap tm_pq;  // int64 elements (Q, P),  dims {pq_cols, out_rows, batch},     box {TW, G, 1}
   int pq_cols;        // strips * TW
-  unsigned long long* prof;  // optional phase-cycle counters (FBF_PROF=1 diagnostics), else null
-  int expt;                  // diagnostics switch (FBF_EXPT), 0 in production
   Geometry g;
   Harmonics h;
   Taps k;
