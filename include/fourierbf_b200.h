@@ -99,6 +99,10 @@ int fbf_launches_per_call(const fbf_filter* f, int variant);
 int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const float* src,
                             float* dst, int variant, long long* bad_index);
 
+/* The host entry points reuse one stream and one device buffer per calling
+ * thread; this frees the calling thread's. */
+void fbf_release_host_buffers(void);
+
 /* Same on fp64 host buffers (the reference Image stores doubles). */
 int fbf_bilateral_fast_host_f64(const fbf_geometry* g, const fbf_filter* f, const double* src,
                                 double* dst, int variant, long long* bad_index);

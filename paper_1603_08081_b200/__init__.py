@@ -82,6 +82,7 @@ SIGNATURES = {
     "fbf_synth_image": (ctypes.c_int, [ctypes.c_ulonglong, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_double, ctypes.c_int, ctypes.c_int, _F, ctypes.c_int]),
     "fbf_probe_fma_peak": (ctypes.c_int, [_D, _D, _P]),
+    "fbf_release_host_buffers": (None, []),
 }
 
 

@@ -15,7 +15,7 @@
 #include "fourierbf_b200.h"
 
 namespace fbf {
-bool fused_supported(int W);
+bool fused_supported(int W, bool box);
 cudaError_t launch_fused(const FusedArgs& a, cudaStream_t st, int* grid_out);
 }  // namespace fbf
 
@@ -41,6 +41,53 @@ int cuda_fail(cudaError_t e, const char* where) {
   } while (0)
 
 size_t align256(size_t n) { return (n + 255) & ~size_t(255); }
+
+// The synchronous host entry points keep one stream and one grow-only device
+// buffer per calling thread (and device): no allocation, stream creation or
+// pool trimming inside repeated calls.  fbf_release_host_buffers() frees them.
+struct HostCtx {
+  int dev = -1;
+  cudaStream_t st = nullptr;
+  char* buf = nullptr;
+  size_t cap = 0;
+};
+thread_local HostCtx g_host;
+thread_local float* g_pinned = nullptr;  // fp32 staging for the fp64 entry points
+thread_local size_t g_pinned_cap = 0;
+
+int host_staging(size_t bytes, float*& out) {
+  if (g_pinned_cap < bytes) {
+    if (g_pinned) cudaFreeHost(g_pinned);
+    g_pinned = nullptr;
+    g_pinned_cap = 0;
+    FBF_CUDA(cudaMallocHost(reinterpret_cast<void**>(&g_pinned), bytes));
+    g_pinned_cap = bytes;
+  }
+  out = g_pinned;
+  return FBF_OK;
+}
+
+int host_ctx(size_t bytes, HostCtx*& out) {
+  int dev = 0;
+  FBF_CUDA(cudaGetDevice(&dev));
+  if (g_host.dev != dev) {  // first call on this thread, or the thread switched devices
+    g_host = HostCtx{};
+    g_host.dev = dev;
+    FBF_CUDA(cudaStreamCreateWithFlags(&g_host.st, cudaStreamNonBlocking));
+  }
+  if (g_host.cap < bytes) {
+    if (g_host.buf) {
+      cudaStreamSynchronize(g_host.st);
+      cudaFree(g_host.buf);
+      g_host.buf = nullptr;
+      g_host.cap = 0;
+    }
+    FBF_CUDA(cudaMalloc(reinterpret_cast<void**>(&g_host.buf), bytes));
+    g_host.cap = bytes;
+  }
+  out = &g_host;
+  return FBF_OK;
+}
 
 // ---------------------------------------------------------------------------
 // prep: (u, f') per source pixel.  u = round(f' * omega/(2 pi) * 2^32) mod 2^32
@@ -382,7 +429,14 @@ void fbf_geometry_whole(fbf_geometry* g, int width, int height, int batch) {
 
 size_t fbf_workspace_bytes(const fbf_geometry* g, int radius, int variant) {
   if (check_geometry(g) != FBF_OK || radius < 1 || radius > kMaxW) return 0;
-  if (variant == FBF_VARIANT_FUSED && !fused_supported(radius)) variant = FBF_VARIANT_NAIVE;
+  if (variant == FBF_VARIANT_FUSED) {
+    const bool g_ok = fused_supported(radius, false), b_ok = fused_supported(radius, true);
+    if (!g_ok && !b_ok) variant = FBF_VARIANT_NAIVE;
+    // the window kind is not known here: cover both paths when they differ
+    if (g_ok != b_ok)
+      return std::max(layout_of(g, radius, FBF_VARIANT_FUSED).total,
+                      layout_of(g, radius, FBF_VARIANT_NAIVE).total);
+  }
   return layout_of(g, radius, variant).total;
 }
 
@@ -405,7 +459,7 @@ int prepare_common(const fbf_geometry* gp, const fbf_filter* f, void* workspace,
   if (rc) return rc;
   if ((rc = check_filter(f))) return rc;
   if ((rc = check_halo(gp, f->radius))) return rc;
-  if (variant == FBF_VARIANT_FUSED && !fused_supported(f->radius)) variant = FBF_VARIANT_NAIVE;
+  if (variant == FBF_VARIANT_FUSED && !fused_supported(f->radius, f->kind == FBF_SPATIAL_BOX)) variant = FBF_VARIANT_NAIVE;
   P.L = layout_of(gp, f->radius, variant);
   if (!workspace || workspace_bytes < P.L.total)
     return fail(FBF_EINVAL, variant == FBF_VARIANT_NAIVE
@@ -498,7 +552,7 @@ int fbf_bilateral_fast_device(const fbf_geometry* gp, const fbf_filter* f, const
 
 int fbf_launches_per_call(const fbf_filter* f, int variant) {
   if (!f) return 0;
-  if (variant == FBF_VARIANT_FUSED && fused_supported(f->radius)) return 2;
+  if (variant == FBF_VARIANT_FUSED && fused_supported(f->radius, f->kind == FBF_SPATIAL_BOX)) return 2;
   return 1 + 4 * (f->N + 1) + 1;
 }
 
@@ -509,7 +563,7 @@ int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const fl
   if ((rc = check_filter(f))) return rc;
   if ((rc = check_halo(g, f->radius))) return rc;
   int v = variant;
-  if (v == FBF_VARIANT_FUSED && !fused_supported(f->radius)) v = FBF_VARIANT_NAIVE;
+  if (v == FBF_VARIANT_FUSED && !fused_supported(f->radius, f->kind == FBF_SPATIAL_BOX)) v = FBF_VARIANT_NAIVE;
   // device buffers: dense copies of the source rows and output rows
   fbf_geometry gd = *g;
   gd.src_pitch = g->width;
@@ -519,15 +573,12 @@ int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const fl
   const size_t src_bytes = static_cast<size_t>(gd.src_bstride) * g->batch * sizeof(float);
   const size_t dst_bytes = static_cast<size_t>(gd.dst_bstride) * g->batch * sizeof(float);
   const size_t ws_bytes = layout_of(&gd, f->radius, v).total;
-  cudaStream_t st;
-  FBF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  char* buf = nullptr;
   const size_t total = align256(src_bytes) + align256(dst_bytes) + ws_bytes + 256;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&buf), total, st);
-  if (e != cudaSuccess) {
-    cudaStreamDestroy(st);
-    return cuda_fail(e, "cudaMallocAsync");
-  }
+  HostCtx* ctx = nullptr;
+  if ((rc = host_ctx(total, ctx))) return rc;
+  cudaStream_t st = ctx->st;
+  char* buf = ctx->buf;
+  cudaError_t e = cudaSuccess;
   float* d_src = reinterpret_cast<float*>(buf);
   float* d_dst = reinterpret_cast<float*>(buf + align256(src_bytes));
   void* ws = buf + align256(src_bytes) + align256(dst_bytes);
@@ -567,10 +618,17 @@ int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const fl
                      std::to_string(x) + ", " + std::to_string(y) + ")");
     }
   } while (false);
-  cudaFreeAsync(buf, st);
   cudaStreamSynchronize(st);
-  cudaStreamDestroy(st);
   return out;
+}
+
+void fbf_release_host_buffers(void) {
+  if (g_host.buf) cudaFree(g_host.buf);
+  if (g_host.st) cudaStreamDestroy(g_host.st);
+  g_host = HostCtx{};
+  if (g_pinned) cudaFreeHost(g_pinned);
+  g_pinned = nullptr;
+  g_pinned_cap = 0;
 }
 
 int fbf_bilateral_fast_host_f64(const fbf_geometry* g, const fbf_filter* f, const double* src,
@@ -587,13 +645,8 @@ int fbf_bilateral_fast_host_f64(const fbf_geometry* g, const fbf_filter* f, cons
   const size_t ns = static_cast<size_t>(gd.src_bstride) * g->batch;
   const size_t nd = static_cast<size_t>(gd.dst_bstride) * g->batch;
   float* hs = nullptr;
-  float* hd = nullptr;
-  FBF_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hs), ns * sizeof(float)));
-  cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&hd), nd * sizeof(float));
-  if (e != cudaSuccess) {
-    cudaFreeHost(hs);
-    return cuda_fail(e, "cudaMallocHost");
-  }
+  if ((rc = host_staging((ns + nd) * sizeof(float), hs))) return rc;
+  float* hd = hs + ns;
   for (int b = 0; b < g->batch; ++b)
     for (int y = 0; y < g->src_rows; ++y)
       for (int x = 0; x < g->width; ++x)
@@ -606,8 +659,6 @@ int fbf_bilateral_fast_host_f64(const fbf_geometry* g, const fbf_filter* f, cons
         for (int x = 0; x < g->width; ++x)
           dst[b * g->dst_bstride + y * g->dst_pitch + x] =
               hd[b * gd.dst_bstride + static_cast<long long>(y) * g->width + x];
-  cudaFreeHost(hs);
-  cudaFreeHost(hd);
   return rc;
 }
 
@@ -636,16 +687,15 @@ int fbf_convolve_host_f64(int width, int height, const double* profile, int radi
                           const double* src, double* dst) {
   if (width <= 0 || height <= 0) return fail(FBF_EINVAL, "convolve: empty plane");
   const size_t n = static_cast<size_t>(width) * height;
-  cudaStream_t st;
-  FBF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   float* h = nullptr;
-  char* d = nullptr;
-  cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&h), n * sizeof(float));
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&d), 3 * align256(n * 4), st);
-  int rc = FBF_OK;
-  if (e != cudaSuccess) {
-    rc = cuda_fail(e, "alloc");
-  } else {
+  HostCtx* ctx = nullptr;
+  int rc = host_staging(n * sizeof(float), h);
+  if (rc == FBF_OK) rc = host_ctx(3 * align256(n * 4), ctx);
+  if (rc) return rc;
+  cudaStream_t st = ctx->st;
+  char* d = ctx->buf;
+  cudaError_t e = cudaSuccess;
+  {
     for (size_t i = 0; i < n; ++i) h[i] = static_cast<float>(src[i]);
     float* ds = reinterpret_cast<float*>(d);
     float* dd = reinterpret_cast<float*>(d + align256(n * 4));
@@ -663,11 +713,8 @@ int fbf_convolve_host_f64(int width, int height, const double* profile, int radi
     } else {
       rc = cuda_fail(e, "convolve H2D");
     }
-    cudaFreeAsync(d, st);
   }
   cudaStreamSynchronize(st);
-  if (h) cudaFreeHost(h);
-  cudaStreamDestroy(st);
   return rc;
 }
 

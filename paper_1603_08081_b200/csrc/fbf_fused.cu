@@ -1,21 +1,30 @@
-// fbf_fused.cu -- radius dispatch for the fused kernel (instantiations live in
-// fbf_fused_w<W>.cu, one translation unit per radius).
+// fbf_fused.cu -- (radius, window kind) dispatch for the fused kernel
+// (instantiations live in fbf_fused_w<W>.cu and fbf_fused_box.cu, one
+// translation unit each so the build parallelises).
 #include "fbf_fused.cuh"
 
 namespace fbf {
 
-extern template cudaError_t launch_w<3>(const FusedArgs&, cudaStream_t, int*);
-extern template cudaError_t launch_w<5>(const FusedArgs&, cudaStream_t, int*);
-extern template cudaError_t launch_w<6>(const FusedArgs&, cudaStream_t, int*);
-extern template cudaError_t launch_w<8>(const FusedArgs&, cudaStream_t, int*);
-extern template cudaError_t launch_w<9>(const FusedArgs&, cudaStream_t, int*);
-extern template cudaError_t launch_w<12>(const FusedArgs&, cudaStream_t, int*);
-extern template cudaError_t launch_w<15>(const FusedArgs&, cudaStream_t, int*);
-extern template cudaError_t launch_w<24>(const FusedArgs&, cudaStream_t, int*);
+#define FBF_EXTERN(WW, BB) extern template cudaError_t launch_w<WW, BB>(const FusedArgs&, cudaStream_t, int*);
+FBF_EXTERN(3, false)
+FBF_EXTERN(5, false)
+FBF_EXTERN(6, false)
+FBF_EXTERN(8, false)
+FBF_EXTERN(9, false)
+FBF_EXTERN(12, false)
+FBF_EXTERN(15, false)
+FBF_EXTERN(24, false)
+FBF_EXTERN(2, true)
+FBF_EXTERN(3, true)
+FBF_EXTERN(4, true)
+FBF_EXTERN(5, true)
+#undef FBF_EXTERN
 
-// Radii with a compiled fused kernel (the BASELINE configs' W=5,9,12,15,24 and
-// the reference tests' W=3,6,8).  Other radii take the naive multi-kernel path.
-bool fused_supported(int W) {
+// Gaussian radii with a compiled fused kernel: the BASELINE configs' 5, 9, 12,
+// 15, 24 and the reference tests' 3, 6, 8.  Box windows: radii 2..5 (c3 is 5),
+// with running-sum passes.  Everything else takes the naive multi-kernel path.
+bool fused_supported(int W, bool box) {
+  if (box) return W >= 2 && W <= 5;
   switch (W) {
     case 3: case 5: case 6: case 8: case 9: case 12: case 15: case 24:
       return true;
@@ -25,6 +34,15 @@ bool fused_supported(int W) {
 }
 
 cudaError_t launch_fused(const FusedArgs& a, cudaStream_t st, int* grid_out) {
+  if (a.k.box) {
+    switch (a.k.W) {
+      case 2: return launch_w<2, true>(a, st, grid_out);
+      case 3: return launch_w<3, true>(a, st, grid_out);
+      case 4: return launch_w<4, true>(a, st, grid_out);
+      case 5: return launch_w<5, true>(a, st, grid_out);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (a.k.W) {
     case 3: return launch_w<3>(a, st, grid_out);
     case 5: return launch_w<5>(a, st, grid_out);

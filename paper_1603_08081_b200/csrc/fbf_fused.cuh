@@ -34,9 +34,13 @@
 
 namespace fbf {
 
-template <int W_, int TW_, int G_, int KR_, int KC_, int NT_>
+// BOX: uniform window -> O(1) running sums (2 adds per output per pass in the
+// steady state) instead of the (2W+1)-tap FIR; the 1/(2W+1)^2 weight is applied
+// once, in the demodulation.
+template <int W_, int TW_, int G_, int KR_, int KC_, int NT_, bool BOX_ = false>
 struct FusedCfg {
   static constexpr int W = W_, TW = TW_, G = G_, KR = KR_, KC = KC_, NT = NT_;
+  static constexpr bool BOX = BOX_;
   static constexpr int MW = TW + 2 * W;   // modulated row width
   static constexpr int MP = MW | 1;       // M pitch in 16-byte units (odd: conflict-free column walks)
   static constexpr int RING = 2 * W + G;  // R ring rows
@@ -156,22 +160,46 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const ulonglong2* _
   const int slot = rel % C::RING;
   const int cslot = rel % C::CRING;
   p2 accA[C::KR], accB[C::KR];
+  if constexpr (C::BOX) {
+    // running sum over the window [i, i+2W] (unweighted)
+    p2 sA = 0ull, sB = 0ull;
 #pragma unroll
-  for (int i = 0; i < C::KR; ++i) accA[i] = accB[i] = 0ull;
-#pragma unroll
-  for (int m = 0; m < C::KR + 2 * C::W; ++m) {
-    const ulonglong2 v = src[m];
-#pragma unroll
-    for (int i = 0; i < C::KR; ++i) {
-      const int j = m - i;
-      if (j >= 0 && j <= 2 * C::W) {
-        const float tv = A.k.t[j < C::W ? C::W - j : j - C::W];
-        accA[i] = fma2(pk(tv, tv), v.x, accA[i]);
-        accB[i] = fma2(pk(tv, tv), v.y, accB[i]);
-      }
+    for (int m = 0; m <= 2 * C::W; ++m) {
+      const ulonglong2 v = src[m];
+      sA = add2(sA, v.x);
+      sB = add2(sB, v.y);
+      if (m >= C::W && m < C::W + C::KR) CS[cslot * C::CP + xc + (m - C::W)] = pk(lo_of(v.x), lo_of(v.y));
     }
-    if (m >= C::W && m < C::W + C::KR)  // centre (c, s) of output column xc + m - W
-      CS[cslot * C::CP + xc + (m - C::W)] = pk(lo_of(v.x), lo_of(v.y));
+    accA[0] = sA;
+    accB[0] = sB;
+#pragma unroll
+    for (int i = 1; i < C::KR; ++i) {
+      const ulonglong2 vin = src[i + 2 * C::W], vout = src[i - 1];
+      sA = sub2(add2(sA, vin.x), vout.x);
+      sB = sub2(add2(sB, vin.y), vout.y);
+      accA[i] = sA;
+      accB[i] = sB;
+      if (i + 2 * C::W >= C::W && i + 2 * C::W < C::W + C::KR)
+        CS[cslot * C::CP + xc + (i + C::W)] = pk(lo_of(vin.x), lo_of(vin.y));
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < C::KR; ++i) accA[i] = accB[i] = 0ull;
+#pragma unroll
+    for (int m = 0; m < C::KR + 2 * C::W; ++m) {
+      const ulonglong2 v = src[m];
+#pragma unroll
+      for (int i = 0; i < C::KR; ++i) {
+        const int j = m - i;
+        if (j >= 0 && j <= 2 * C::W) {
+          const float tv = A.k.t[j < C::W ? C::W - j : j - C::W];
+          accA[i] = fma2(pk(tv, tv), v.x, accA[i]);
+          accB[i] = fma2(pk(tv, tv), v.y, accB[i]);
+        }
+      }
+      if (m >= C::W && m < C::W + C::KR)  // centre (c, s) of output column xc + m - W
+        CS[cslot * C::CP + xc + (m - C::W)] = pk(lo_of(v.x), lo_of(v.y));
+    }
   }
   ulonglong2* __restrict__ dst = R + slot * C::RP + xc;
 #pragma unroll
@@ -188,33 +216,60 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const ulonglong2* _
   const int gx = u.x0 + x;
   const int nr = min(C::KC, u.y1 - r0);  // <= 0: this thread only helps with the modulation
   p2 accA[C::KC], accB[C::KC];
-#pragma unroll
-  for (int i = 0; i < C::KC; ++i) accA[i] = accB[i] = 0ull;
   const int s0 = (r0 - C::W - base) % C::RING;
   constexpr int TAPS_IN = C::KC + 2 * C::W;
   constexpr int ELEMS = ModNext<C>::ELEMS;
   constexpr int STRIDE = TAPS_IN / ELEMS > 0 ? TAPS_IN / ELEMS : 1;
-#pragma unroll
-  for (int m = 0; m < TAPS_IN; ++m) {
+  auto ring = [&](int m) {
     int s = s0 + m;
     s = s >= C::RING ? s - C::RING : s;
-    const ulonglong2 v = R[s * C::RP + x];
+    return R[s * C::RP + x];
+  };
+  if constexpr (C::BOX) {
+    p2 sA = 0ull, sB = 0ull;
 #pragma unroll
-    for (int i = 0; i < C::KC; ++i) {
-      const int j = m - i;
-      if (j >= 0 && j <= 2 * C::W) {
-        const float tv = A.k.t[j < C::W ? C::W - j : j - C::W];
-        accA[i] = fma2(pk(tv, tv), v.x, accA[i]);
-        accB[i] = fma2(pk(tv, tv), v.y, accB[i]);
-      }
+    for (int m = 0; m <= 2 * C::W; ++m) {
+      const ulonglong2 v = ring(m);
+      sA = add2(sA, v.x);
+      sB = add2(sB, v.y);
+      if (m % STRIDE == 0 && m / STRIDE < ELEMS) next.element(m / STRIDE);
     }
-    // one slice of the next step's modulation per STRIDE taps
-    if (m % STRIDE == 0 && m / STRIDE < ELEMS) next.element(m / STRIDE);
+    accA[0] = sA;
+    accB[0] = sB;
+#pragma unroll
+    for (int i = 1; i < C::KC; ++i) {
+      const ulonglong2 vin = ring(i + 2 * C::W), vout = ring(i - 1);
+      sA = sub2(add2(sA, vin.x), vout.x);
+      sB = sub2(add2(sB, vin.y), vout.y);
+      accA[i] = sA;
+      accB[i] = sB;
+      const int m = i + 2 * C::W;
+      if (m % STRIDE == 0 && m / STRIDE < ELEMS) next.element(m / STRIDE);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < C::KC; ++i) accA[i] = accB[i] = 0ull;
+#pragma unroll
+    for (int m = 0; m < TAPS_IN; ++m) {
+      const ulonglong2 v = ring(m);
+#pragma unroll
+      for (int i = 0; i < C::KC; ++i) {
+        const int j = m - i;
+        if (j >= 0 && j <= 2 * C::W) {
+          const float tv = A.k.t[j < C::W ? C::W - j : j - C::W];
+          accA[i] = fma2(pk(tv, tv), v.x, accA[i]);
+          accB[i] = fma2(pk(tv, tv), v.y, accB[i]);
+        }
+      }
+      // one slice of the next step's modulation per STRIDE taps
+      if (m % STRIDE == 0 && m / STRIDE < ELEMS) next.element(m / STRIDE);
+    }
   }
 #pragma unroll
   for (int k = TAPS_IN / STRIDE + (TAPS_IN % STRIDE ? 1 : 0); k < ELEMS; ++k) next.element(k);
   if (nr <= 0 || gx >= A.g.width) return;
-  const float dn = A.h.d[n];
+  // box: both passes summed unweighted; the weight (1/(2W+1))^2 = w0 joins d_n here
+  const float dn = C::BOX ? A.h.d[n] * (A.k.box_tap * A.k.box_tap) : A.h.d[n];
   const p2 dd = pk(dn, dn);
   const bool last = (n == A.h.N);
   const int cs0 = (r0 - base) % C::CRING;
@@ -284,8 +339,17 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
   unsigned ph_uf = 0, ph_pq = 0;  // phase parity of the next completion of each barrier
 
   const long long total = A.total;
-  const long long lo = total * blockIdx.x / gridDim.x;
-  const long long hi = total * (blockIdx.x + 1) / gridDim.x;
+  // CTA ranges in (strip, row) space, with the row rounded down to a multiple
+  // of KC: every column-pass block then starts at the same row offset whatever
+  // the partition (the box path's running sums are order-sensitive), so the
+  // result is bit-identical across CTA counts and multi-GPU strip splits.
+  auto split = [&](long long p) {
+    const long long sidx = p / A.g.out_rows;
+    const long long r = p - sidx * A.g.out_rows;
+    return sidx * A.g.out_rows + (r - r % C::KC);
+  };
+  const long long lo = blockIdx.x == 0 ? 0 : split(total * blockIdx.x / gridDim.x);
+  const long long hi = blockIdx.x + 1 == gridDim.x ? total : split(total * (blockIdx.x + 1) / gridDim.x);
   for (long long pos = lo; pos < hi;) {
     const long long sidx = pos / A.g.out_rows;
     const int r0 = static_cast<int>(pos - sidx * A.g.out_rows);
@@ -410,10 +474,10 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
 // Small (128 threads, G=16, two CTAs per SM) for W <= 9, big (256 threads,
 // G=32, one CTA per SM) otherwise -- measured, profiles/r01_cfg_compare.txt.
 // FBF_FUSED_CFG=small|big overrides where both fit (experiments).
-template <int W>
+template <int W, bool BOX = false>
 cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
-  using Small = FusedCfg<W, 64, 16, 8, 8, 128>;
-  using Big = FusedCfg<W, 64, 32, 8, 8, 256>;
+  using Small = FusedCfg<W, 64, 16, 8, 8, 128, BOX>;
+  using Big = FusedCfg<W, 64, 32, 8, 8, 256, BOX>;
   if constexpr (Small::smem_bytes <= 113 * 1024) {
     const char* env = getenv("FBF_FUSED_CFG");
     const bool big = env ? env[0] == 'b' : !(W <= 9);
@@ -425,4 +489,6 @@ cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
 }  // namespace fbf
 
 #define FBF_INSTANTIATE_FUSED(WW) \
-  template cudaError_t fbf::launch_w<WW>(const fbf::FusedArgs&, cudaStream_t, int*);
+  template cudaError_t fbf::launch_w<WW, false>(const fbf::FusedArgs&, cudaStream_t, int*);
+#define FBF_INSTANTIATE_FUSED_BOX(WW) \
+  template cudaError_t fbf::launch_w<WW, true>(const fbf::FusedArgs&, cudaStream_t, int*);

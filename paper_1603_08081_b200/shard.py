@@ -19,6 +19,9 @@ from dataclasses import dataclass
 from typing import List
 
 
+ROW_ALIGN = 8  # = the fused kernel's rows per column-pass block (KC)
+
+
 @dataclass(frozen=True)
 class Shard:
     images: List[int]   # batch indices owned by the rank
@@ -52,7 +55,11 @@ def plan(width: int, height: int, batch: int, radius: int, world: int, rank: int
     if batch > 1:
         b0, b1 = batch * rank // world, batch * (rank + 1) // world
         return Shard(list(range(b0, b1)), 0, height, 0, height)
-    r0, r1 = height * rank // world, height * (rank + 1) // world
+    # cuts on multiples of ROW_ALIGN: the kernel's column-pass blocks then start
+    # at the same global rows as in a single-GPU run (bit-identical results)
+    def cut(k):
+        return 0 if k == 0 else height if k == world else (height * k // world) // ROW_ALIGN * ROW_ALIGN
+    r0, r1 = cut(rank), cut(rank + 1)
     lo, hi = source_rows(r0, r1 - r0, height, radius) if r1 > r0 else (r0, r0)
     return Shard([0], r0, r1 - r0, lo, hi - lo)
 
