@@ -315,7 +315,7 @@ def main():
                                "(128 FP32 lanes x 148 SMs); ops = FP32 FMA-pipe lane ops (FFMA/FMUL/FADD = 1)",
                 "hbm_bytes_per_pixel_algorithmic": 8,
             },
-            "gpu_launches": args.steps * fb.launches_per_call(spatial, approx, args.variant),
+            "gpu_launches": args.steps * fb.launches_per_call(geo, spatial, approx, args.variant),
             "clocks": clk.summary(),
         }
         if e2e:

@@ -92,7 +92,19 @@ int fbf_filter_prepared_device(const fbf_geometry* g, const fbf_filter* f, float
                                void* workspace, size_t workspace_bytes,
                                unsigned long long* d_bad, int variant, void* stream);
 /* Kernel launches one fbf_bilateral_fast_device call makes. */
-int fbf_launches_per_call(const fbf_filter* f, int variant);
+int fbf_launches_per_call(const fbf_geometry* g, const fbf_filter* f, int variant);
+
+/* Harmonic split (SURVEY.md §8(e) optional mode): the partial numerator and
+ * denominator sums over harmonics [n_lo, n_hi) into pq_out, a dense device
+ * array of (Q, P) fp32 pairs (batch x out_rows x width), after
+ * fbf_prepare_device on the same workspace.  Ranks holding disjoint harmonic
+ * ranges sum their pq_out (e.g. NCCL all-reduce) and call fbf_finish_device,
+ * which divides (with the reference's collapse check) into dst. */
+int fbf_partial_sums_device(const fbf_geometry* g, const fbf_filter* f, int n_lo, int n_hi,
+                            float* pq_out, void* workspace, size_t workspace_bytes, int variant,
+                            void* stream);
+int fbf_finish_device(const fbf_geometry* g, const fbf_filter* f, const float* pq, float* dst,
+                      unsigned long long* d_bad, void* stream);
 
 /* Synchronous, host buffers (fp32): H2D, filter, D2H.  On FBF_EANOMALY
  * *bad_index holds the first offending index. */

@@ -261,6 +261,7 @@ typedef struct {
     const double* d; int N; double omega;
     int row0, row1;
     double* P; double* Q;   /* (row1-row0)*w, caller zeroed */
+    int n_lo, n_hi;         /* harmonic range [n_lo, n_hi) */
 } fast_job;
 
 /* source rows needed by output rows [row0,row1): [lo, hi) */
@@ -294,7 +295,7 @@ static void* fast_worker(void* arg) {
     double* pad = (double*)malloc(sizeof(double) * L);
     double conv[4];
 
-    for (int n = 0; n <= J->N; ++n) {
+    for (int n = J->n_lo; n < J->n_hi; ++n) {
         const double freq = J->omega * n;
         for (size_t i = 0; i < sz; ++i) {
             double f = J->img[(size_t)lo * w + i];
@@ -333,6 +334,18 @@ static void* fast_worker(void* arg) {
     return NULL;
 }
 
+/* The numerator/denominator sums of bilateral.hpp:125-145 restricted to the
+ * harmonics [n_lo, n_hi) (the decomposition the multi-GPU harmonic split
+ * distributes): P and Q are (row1-row0)*w, overwritten. */
+void fbo_partial_sums(const double* img, int w, int h, const double* p, int W, const double* d, int N,
+                      double omega, int n_lo, int n_hi, int row0, int row1, double* P, double* Q) {
+    const int no = row1 - row0;
+    memset(P, 0, sizeof(double) * (size_t)no * w);
+    memset(Q, 0, sizeof(double) * (size_t)no * w);
+    fast_job J = {img, w, h, p, W, d, N, omega, row0, row1, P, Q, n_lo, n_hi};
+    fast_worker(&J);
+}
+
 int fbo_bilateral_fast(const double* img, int w, int h, const double* p, int W, double w0,
                        const double* d, int N, double omega, double max_err, int check_eps,
                        int row0, int row1, int nthreads, double* out, long long* bad_index) {
@@ -348,7 +361,7 @@ int fbo_bilateral_fast(const double* img, int w, int h, const double* p, int W, 
     for (int t = 0; t < nthreads; ++t) {
         int a = row0 + (int)((long)no * t / nthreads), b = row0 + (int)((long)no * (t + 1) / nthreads);
         fast_job J = {img, w, h, p, W, d, N, omega, a, b,
-                      P + (size_t)(a - row0) * w, Q + (size_t)(a - row0) * w};
+                      P + (size_t)(a - row0) * w, Q + (size_t)(a - row0) * w, 0, N + 1};
         jobs[t] = J;
         if (nthreads > 1) pthread_create(&th[t], NULL, fast_worker, &jobs[t]);
         else fast_worker(&jobs[t]);

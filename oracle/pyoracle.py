@@ -65,6 +65,8 @@ class Oracle:
         L.fbo_bilateral_exact.argtypes = [_D, ctypes.c_int, ctypes.c_int, _D, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D]
         L.fbo_local_dynamic_range.argtypes = [_D, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        L.fbo_partial_sums.argtypes = [_D, ctypes.c_int, ctypes.c_int, _D, ctypes.c_int, _D, ctypes.c_int,
+                                       ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D, _D]
         L.fbo_error_bound.restype = ctypes.c_double
         L.fbo_error_bound.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double]
         self.L = L
@@ -142,6 +144,18 @@ class Oracle:
 
     def error_bound(self, T, eps, w0):
         return self.L.fbo_error_bound(T, eps, w0)
+
+    def partial_sums(self, img, profile, radius, d, omega, n_lo, n_hi, row0=0, row1=None):
+        """(P, Q) over harmonics [n_lo, n_hi)."""
+        a = _f64(img)
+        h, w = a.shape
+        row1 = h if row1 is None else row1
+        P = np.zeros((row1 - row0, w))
+        Q = np.zeros((row1 - row0, w))
+        dd = _f64(d)
+        self.L.fbo_partial_sums(_dp(a), w, h, _dp(_f64(profile)), radius, _dp(dd), len(dd) - 1, omega, n_lo, n_hi,
+                                row0, row1, _dp(P), _dp(Q))
+        return P, Q
 
 
 class Reference:

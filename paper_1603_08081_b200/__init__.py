@@ -64,7 +64,10 @@ SIGNATURES = {
                                           ctypes.c_size_t, ctypes.c_int, _P]),
     "fbf_filter_prepared_device": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.POINTER(Filter), _P, _P,
                                                   ctypes.c_size_t, _P, ctypes.c_int, _P]),
-    "fbf_launches_per_call": (ctypes.c_int, [ctypes.POINTER(Filter), ctypes.c_int]),
+    "fbf_launches_per_call": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.POINTER(Filter), ctypes.c_int]),
+    "fbf_partial_sums_device": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.POINTER(Filter), ctypes.c_int,
+                                               ctypes.c_int, _P, _P, ctypes.c_size_t, ctypes.c_int, _P]),
+    "fbf_finish_device": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.POINTER(Filter), _P, _P, _P, _P]),
     "fbf_bilateral_fast_host": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.POINTER(Filter), _F, _F,
                                                ctypes.c_int, _LL]),
     "fbf_bilateral_fast_host_f64": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.POINTER(Filter), _D, _D,
@@ -282,9 +285,26 @@ def filter_prepared_device(dst_ptr: int, geometry: Geometry, spatial: SpatialKer
                                           workspace_bytes, bad_ptr, _VARIANTS[variant], stream))
 
 
-def launches_per_call(spatial: SpatialKernel, approx: FourierKernelApprox, variant: str = "fused") -> int:
+def launches_per_call(geometry: Geometry, spatial: SpatialKernel, approx: FourierKernelApprox,
+                      variant: str = "fused") -> int:
     f = _filter_struct(spatial, approx)
-    return int(lib.fbf_launches_per_call(ctypes.byref(f), _VARIANTS[variant]))
+    return int(lib.fbf_launches_per_call(ctypes.byref(geometry), ctypes.byref(f), _VARIANTS[variant]))
+
+
+def partial_sums_device(pq_ptr: int, geometry: Geometry, spatial: SpatialKernel, approx: FourierKernelApprox,
+                        n_lo: int, n_hi: int, workspace_ptr: int, workspace_bytes: int, stream: int = 0,
+                        variant: str = "fused", check_epsilon: bool = True) -> None:
+    """(Q, P) partial sums over harmonics [n_lo, n_hi) into a dense float2 device array (after prepare_device)."""
+    f = _filter_struct(spatial, approx, check_epsilon)
+    _check(lib.fbf_partial_sums_device(ctypes.byref(geometry), ctypes.byref(f), int(n_lo), int(n_hi), pq_ptr,
+                                       workspace_ptr, workspace_bytes, _VARIANTS[variant], stream))
+
+
+def finish_device(pq_ptr: int, dst_ptr: int, geometry: Geometry, spatial: SpatialKernel,
+                  approx: FourierKernelApprox, bad_ptr: int, stream: int = 0, check_epsilon: bool = True) -> None:
+    """Divide summed (Q, P) into the output with the reference's denominator-collapse check."""
+    f = _filter_struct(spatial, approx, check_epsilon)
+    _check(lib.fbf_finish_device(ctypes.byref(geometry), ctypes.byref(f), pq_ptr, dst_ptr, bad_ptr, stream))
 
 
 def workspace_bytes(geometry: Geometry, radius: int, variant: str = "fused") -> int:

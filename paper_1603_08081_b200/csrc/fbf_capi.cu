@@ -379,6 +379,59 @@ struct Layout {
   size_t uf, pq, m, t, c, total;
 };
 
+// Harmonic split inside one GPU: the harmonics are divided among CTA groups,
+// each accumulating its own (Q, P) plane, summed in a fixed order at the end.
+// Each group's CTAs get work units with `groups` times more rows, which cuts
+// the per-unit 2W-row prologue by that factor and keeps small images from
+// degenerating into very short units; large images lose to the extra (Q, P)
+// traffic.  Measured (profiles/r01_groups.txt): 8 groups for <= 0.5 Mpx
+// images (c1 1575 -> 3142 Mpx/s), 4 for <= 2 Mpx with W <= 9 (c3 3124 -> 3939),
+// 1 otherwise (c4 -9 %, c5 -17 % at 4).  A function of the GLOBAL image size
+// and the radius only -- never of the strip or batch a shard holds -- so
+// results are bit-identical across multi-GPU partitions.  FBF_GROUPS overrides.
+int harmonic_groups(const fbf_geometry* g, int radius) {
+  static const int forced = [] {
+    const char* e = getenv("FBF_GROUPS");
+    return e ? std::max(1, std::min(8, atoi(e))) : 0;
+  }();
+  if (forced) return forced;
+  const long long px = static_cast<long long>(g->width) * g->height;
+  if (px <= 512LL * 1024) return 8;
+  if (px <= 2LL * 1024 * 1024 && radius <= 9) return 4;
+  return 1;
+}
+
+// sum of the nonempty groups' (Q, P) planes -> divide (or -> a dense plane)
+__global__ void finish_groups(const p2* __restrict__ pq, int groups, int span, long long plane, int pq_cols,
+                              Geometry g, float shift, float q_floor, unsigned long long* bad,
+                              float* __restrict__ dst, p2* __restrict__ sum_out) {
+  const long long per_out = static_cast<long long>(g.out_rows) * g.width;
+  const long long total = per_out * g.batch;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long b = i / per_out;
+    const long long r = i - b * per_out;
+    const int yl = static_cast<int>(r / g.width);
+    const int x = static_cast<int>(r % g.width);
+    const long long at = (b * g.out_rows + yl) * pq_cols + x;
+    p2 acc = 0ull;
+    for (int k = 0; k < groups; ++k)  // fixed order: deterministic
+      if (span * (k + 1) / groups > span * k / groups) acc = add2(acc, pq[k * plane + at]);
+    if (sum_out) {
+      sum_out[i] = acc;
+      continue;
+    }
+    float Q, P;
+    upk(acc, Q, P);
+    if (!(fabsf(Q) >= q_floor) && bad) {
+      const unsigned long long lin = static_cast<unsigned long long>(b) * g.full_height * g.width +
+                                     static_cast<unsigned long long>(g.out_row0 + yl) * g.width + x;
+      atomicMin(bad, lin);
+    }
+    dst[b * g.dst_bstride + static_cast<long long>(yl) * g.dst_pitch + x] = shift + __fdiv_rn(P, Q);
+  }
+}
+
 // Fused: mirror-padded (u, f') image (out_rows + 2W) x (strips*TW + 2W) and a
 // (Q, P) plane out_rows x strips*TW per image (see FusedArgs).  Naive: dense
 // (u, f') of the source rows, (Q, P) per output pixel and three float4 planes.
@@ -391,7 +444,8 @@ Layout layout_of(const fbf_geometry* g, int radius, int variant) {
     const size_t cols = static_cast<size_t>((g->width + kFusedTW - 1) / kFusedTW) * kFusedTW;
     const size_t uf_px = static_cast<size_t>(g->batch) * (g->out_rows + 2 * radius) * (cols + 2 * radius);
     L.pq = align256(uf_px * sizeof(int2));
-    L.total = L.pq + align256(static_cast<size_t>(g->batch) * g->out_rows * cols * sizeof(Pair));
+    L.total = L.pq + align256(static_cast<size_t>(harmonic_groups(g, radius)) * g->batch * g->out_rows * cols *
+                              sizeof(Pair));
     return L;
   }
   L.pq = align256(src_px * sizeof(int2));
@@ -519,7 +573,20 @@ int fbf_filter_prepared_device(const fbf_geometry* gp, const fbf_filter* f, floa
     A.pq = P.pq;
     A.bad = d_bad;
     A.seg_max = 1 << 30;
+    A.n_lo = 0;
+    A.n_hi = P.H.N + 1;
+    A.groups = std::min(harmonic_groups(gp, f->radius), P.H.N + 1);
+    A.partial = A.groups > 1;
     FBF_CUDA(launch_fused(A, st, nullptr));
+    if (A.groups > 1) {
+      const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
+      const long long plane = static_cast<long long>(P.G.batch) * P.G.out_rows * cols;
+      const long long out_px = static_cast<long long>(P.G.batch) * P.G.out_rows * P.G.width;
+      finish_groups<<<grid_for(out_px, 256), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), A.groups,
+                                                          A.n_hi - A.n_lo, plane, cols, P.G, P.H.shift,
+                                                          P.H.q_floor, d_bad, dst, nullptr);
+      FBF_CUDA(cudaGetLastError());
+    }
     return FBF_OK;
   }
   // naive: HBM-resident planes, four kernels per harmonic
@@ -550,9 +617,74 @@ int fbf_bilateral_fast_device(const fbf_geometry* gp, const fbf_filter* f, const
   return fbf_filter_prepared_device(gp, f, dst, workspace, workspace_bytes, d_bad, variant, stream);
 }
 
-int fbf_launches_per_call(const fbf_filter* f, int variant) {
-  if (!f) return 0;
-  if (variant == FBF_VARIANT_FUSED && fused_supported(f->radius, f->kind == FBF_SPATIAL_BOX)) return 2;
+int fbf_partial_sums_device(const fbf_geometry* gp, const fbf_filter* f, int n_lo, int n_hi, float* pq_out,
+                            void* workspace, size_t workspace_bytes, int variant, void* stream) {
+  Prepared P;
+  int rc = prepare_common(gp, f, workspace, workspace_bytes, variant, P);
+  if (rc) return rc;
+  if (n_lo < 0 || n_hi > P.H.N + 1 || n_lo >= n_hi || !pq_out)
+    return fail(FBF_EINVAL, "partial_sums: harmonic range outside [0, N]");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const long long out_px = static_cast<long long>(P.G.batch) * P.G.out_rows * P.G.width;
+  if (P.variant == FBF_VARIANT_FUSED) {
+    FusedArgs A;
+    std::memset(&A, 0, sizeof(A));
+    A.g = P.Gd;
+    A.h = P.H;
+    A.k = P.K;
+    A.uf = P.uf;
+    A.pq = P.pq;
+    A.seg_max = 1 << 30;
+    A.n_lo = n_lo;
+    A.n_hi = n_hi;
+    A.groups = std::min(harmonic_groups(gp, f->radius), n_hi - n_lo);
+    A.partial = 1;
+    FBF_CUDA(launch_fused(A, st, nullptr));
+    const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
+    const long long plane = static_cast<long long>(P.G.batch) * P.G.out_rows * cols;
+    finish_groups<<<grid_for(out_px, 256), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), A.groups,
+                                                        n_hi - n_lo, plane, cols, P.G, 0.f, 0.f, nullptr,
+                                                        nullptr, reinterpret_cast<p2*>(pq_out));
+    FBF_CUDA(cudaGetLastError());
+    return FBF_OK;
+  }
+  ulonglong2* M = reinterpret_cast<ulonglong2*>(P.ws + P.L.m);
+  ulonglong2* T = reinterpret_cast<ulonglong2*>(P.ws + P.L.t);
+  ulonglong2* Cc = reinterpret_cast<ulonglong2*>(P.ws + P.L.c);
+  NaiveArgs NA;
+  NA.g = P.Gd;
+  NA.k = P.K;
+  const long long src_px = static_cast<long long>(P.G.batch) * P.G.src_rows * P.G.width;
+  for (int n = n_lo; n < n_hi; ++n) {
+    naive_modulate<<<grid_for(src_px, 256), 256, 0, st>>>(P.uf, M, src_px, static_cast<uint32_t>(n));
+    naive_rows<<<grid_for(src_px, 256), 256, 0, st>>>(M, T, NA);
+    naive_cols<<<grid_for(out_px, 256), 256, 0, st>>>(T, Cc, NA);
+    naive_demod<<<grid_for(out_px, 256), 256, 0, st>>>(M, Cc, reinterpret_cast<p2*>(pq_out), P.Gd, P.H.d[n],
+                                                       n == n_lo);
+  }
+  FBF_CUDA(cudaGetLastError());
+  return FBF_OK;
+}
+
+int fbf_finish_device(const fbf_geometry* gp, const fbf_filter* f, const float* pq, float* dst,
+                      unsigned long long* d_bad, void* stream) {
+  int rc = check_geometry(gp);
+  if (rc) return rc;
+  if ((rc = check_filter(f))) return rc;
+  Harmonics H;
+  fill_harmonics(H, f);
+  const Geometry G = to_geometry(gp);
+  const long long out_px = static_cast<long long>(G.batch) * G.out_rows * G.width;
+  finish_kernel<<<grid_for(out_px, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const p2*>(pq), dst, G, H.shift, H.q_floor, d_bad);
+  FBF_CUDA(cudaGetLastError());
+  return FBF_OK;
+}
+
+int fbf_launches_per_call(const fbf_geometry* g, const fbf_filter* f, int variant) {
+  if (!f || !g) return 0;
+  if (variant == FBF_VARIANT_FUSED && fused_supported(f->radius, f->kind == FBF_SPATIAL_BOX))
+    return std::min(harmonic_groups(g, f->radius), f->N + 1) > 1 ? 3 : 2;  // prep, fused (, group sum)
   return 1 + 4 * (f->N + 1) + 1;
 }
 

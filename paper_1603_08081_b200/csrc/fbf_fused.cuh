@@ -106,7 +106,7 @@ __device__ __forceinline__ void tma_uf(const FusedArgs& A, int2* stage, uint64_t
 template <class C>
 __device__ __forceinline__ void tma_pq(const FusedArgs& A, p2* pqs, uint64_t* bar, const Unit& u, int o) {
   mbar_expect_tx(bar, static_cast<unsigned>(C::G * C::TW * 8));
-  tma_load_3d(pqs, &A.tm_pq, bar, u.x0, o - A.g.out_row0, u.b);
+  tma_load_3d(pqs, &A.tm_pq, bar, u.x0, o - A.g.out_row0, static_cast<int>(blockIdx.y) * A.g.batch + u.b);
 }
 
 // Modulation of one step, sliced into RPW*NJ independent elements per thread.
@@ -209,7 +209,8 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const ulonglong2* _
 template <class C>
 __device__ __forceinline__ void col_pass(const FusedArgs& A, const ulonglong2* __restrict__ R,
                                          const p2* __restrict__ CS, const p2* __restrict__ pqs,
-                                         const Unit& u, int o, int base, int n, const ModNext<C>& next) {
+                                         const Unit& u, int o, int base, int n, bool first, bool divide,
+                                         const ModNext<C>& next) {
   const int x = threadIdx.x % C::TW;
   const int gi = (threadIdx.x / C::TW) * C::KC;  // first output row of this thread, rel. to o
   const int r0 = o + gi;
@@ -271,10 +272,10 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const ulonglong2* _
   // box: both passes summed unweighted; the weight (1/(2W+1))^2 = w0 joins d_n here
   const float dn = C::BOX ? A.h.d[n] * (A.k.box_tap * A.k.box_tap) : A.h.d[n];
   const p2 dd = pk(dn, dn);
-  const bool last = (n == A.h.N);
   const int cs0 = (r0 - base) % C::CRING;
   p2* __restrict__ pqrow = reinterpret_cast<p2*>(A.pq) +
-                           (u.b * static_cast<long long>(A.g.out_rows) + (r0 - A.g.out_row0)) * A.pq_cols + gx;
+                           ((blockIdx.y * A.g.batch + u.b) * static_cast<long long>(A.g.out_rows) +
+                            (r0 - A.g.out_row0)) * A.pq_cols + gx;
   const int wstride = A.pq_cols;
   // demodulate all KC outputs straight-line; only the global stores are predicated
   p2 qp[C::KC];
@@ -287,8 +288,8 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const ulonglong2* _
     // (q, p) = c (Gc, Fc) + s (Gs, Fs)   [bilateral.hpp:138-144, real form]
     qp[i] = fma2(pk(s, s), accB[i], mul2(pk(c, c), accA[i]));
   }
-  if (!last) {
-    if (n == 0) {
+  if (!divide) {
+    if (first) {
 #pragma unroll
       for (int i = 0; i < C::KC; ++i)
         if (i < nr) pqrow[i * wstride] = mul2(dd, qp[i]);
@@ -305,7 +306,7 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const ulonglong2* _
 #pragma unroll
   for (int i = 0; i < C::KC; ++i) {
     if (i < nr) {
-      const p2 acc = (n == 0) ? mul2(dd, qp[i]) : fma2(dd, qp[i], pqs[(gi + i) * C::TW + x]);
+      const p2 acc = first ? mul2(dd, qp[i]) : fma2(dd, qp[i], pqs[(gi + i) * C::TW + x]);
       float Q, P;
       upk(acc, Q, P);
       if (!(fabsf(Q) >= A.h.q_floor) && A.bad) {
@@ -337,6 +338,11 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
   }
   __syncthreads();
   unsigned ph_uf = 0, ph_pq = 0;  // phase parity of the next completion of each barrier
+  // this CTA group's harmonics [nb, ne)
+  const int span = A.n_hi - A.n_lo;
+  const int nb = A.n_lo + span * static_cast<int>(blockIdx.y) / A.groups;
+  const int ne = A.n_lo + span * static_cast<int>(blockIdx.y + 1) / A.groups;
+  if (nb >= ne) return;
 
   const long long total = A.total;
   // CTA ranges in (strip, row) space, with the row rounded down to a multiple
@@ -363,7 +369,7 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
     const int base = u.y0 - C::W;
     const int nsteps = C::PROLOGUE + (len + C::G - 1) / C::G;
 
-    {  // bootstrap: step 0 of harmonic 0 into M
+    {  // bootstrap: step 0 of the group's first harmonic into M
       int a, rows, o;
       step_rows<C>(u, 0, a, rows, o);
       __syncthreads();  // the previous unit finished reading stage and M
@@ -373,15 +379,17 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
       }
       mbar_wait(bar_uf, ph_uf);
       ph_uf ^= 1u;
-      modulate_rows<C>(stage, M, rows, 0u);
+      modulate_rows<C>(stage, M, rows, static_cast<uint32_t>(nb));
     }
-    for (int n = 0; n <= A.h.N; ++n) {
+    for (int n = nb; n < ne; ++n) {
+      const bool first = n == nb;
+      const bool divide = n + 1 == ne && !A.partial;
       for (int s = 0; s < nsteps; ++s) {
         int a, rows, o, a2, rows2, o2;
         step_rows<C>(u, s, a, rows, o);
         const bool wrap = s + 1 == nsteps;  // next step is step 0 of harmonic n+1
-        const bool more = !wrap || n < A.h.N;
-        const bool want_pq = o >= 0 && n > 0;
+        const bool more = !wrap || n + 1 < ne;
+        const bool want_pq = o >= 0 && !first;
         step_rows<C>(u, wrap ? 0 : s + 1, a2, rows2, o2);
         __syncthreads();  // S1: M holds this step; the previous column pass is done; stage free
         if (leader) {
@@ -403,7 +411,7 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
         // (its ALU work issues in the FFMA2 shadow); prologue steps run it alone
         const ModNext<C> next{stage, M, static_cast<uint32_t>(wrap ? n + 1 : n)};
         if (o >= 0)
-          col_pass<C>(A, R, CS, pqs, u, o, base, n, next);
+          col_pass<C>(A, R, CS, pqs, u, o, base, n, first, divide, next);
         else
           modulate_rows<C>(stage, M, rows2, next.n);
       }
@@ -448,9 +456,10 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
                                  static_cast<unsigned long long>(a.g.out_rows + 2 * W),
                                  static_cast<unsigned long long>(a.g.batch), C::MW, C::G);
   if (e != cudaSuccess) return e;
+  if (a.groups < 1) a.groups = 1;
   e = encode_tile_3d(&a.tm_pq, a.pq, static_cast<unsigned long long>(a.pq_cols),
-                     static_cast<unsigned long long>(a.g.out_rows), static_cast<unsigned long long>(a.g.batch),
-                     C::TW, C::G);
+                     static_cast<unsigned long long>(a.g.out_rows),
+                     static_cast<unsigned long long>(a.g.batch) * a.groups, C::TW, C::G);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(fused_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(C::smem_bytes));
@@ -460,14 +469,15 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel<C>, C::NT, C::smem_bytes);
   if (occ < 1) occ = 1;
-  long long grid = static_cast<long long>(sms) * occ;
+  // one wave in total: the harmonic groups share the SMs
+  long long grid = (static_cast<long long>(sms) * occ + a.groups - 1) / a.groups;
   // keep at least ~2W+G rows per CTA so the per-unit prologue stays amortised
   const long long min_rows = 2 * C::W + C::G;
   const long long by_work = (a.total + min_rows - 1) / min_rows;
   if (grid > by_work) grid = by_work;
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = static_cast<int>(grid);
-  fused_kernel<C><<<static_cast<unsigned>(grid), C::NT, C::smem_bytes, st>>>(a);
+  fused_kernel<C><<<dim3(static_cast<unsigned>(grid), static_cast<unsigned>(a.groups)), C::NT, C::smem_bytes, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -54,6 +54,14 @@ struct FusedArgs {
   CUtensorMap tm_uf;  // int64 elements (u, f'), dims {uf_cols, out_rows + 2W, batch}, box {TW+2W, G, 1}
   CUtensorMap tm_pq;  // int64 elements (Q, P),  dims {pq_cols, out_rows, batch},     box {TW, G, 1}
   int pq_cols;        // strips * TW
+  // Harmonic split: harmonics [n_lo, n_hi) are divided among `groups` CTA
+  // groups (grid.y); group k accumulates its share into its own (Q, P) plane
+  // (pq + k * batch * out_rows * pq_cols).  With partial = 0 and one group the
+  // kernel divides at the last harmonic; otherwise it leaves the partial sums
+  // in the planes for fbf_finish / an NCCL sum.
+  int n_lo, n_hi;
+  int groups;
+  int partial;
   Geometry g;
   Harmonics h;
   Taps k;

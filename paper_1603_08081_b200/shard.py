@@ -64,6 +64,36 @@ def plan(width: int, height: int, batch: int, radius: int, world: int, rank: int
     return Shard([0], r0, r1 - r0, lo, hi - lo)
 
 
+def harmonic_range(N: int, world: int, rank: int):
+    """[n_lo, n_hi) of the harmonics 0..N assigned to `rank` in the harmonic-split mode."""
+    return (N + 1) * rank // world, (N + 1) * (rank + 1) // world
+
+
+def harmonic_split_filter(src, geo, spatial, approx, workspace, dst, bad, group=None, variant="fused",
+                          check_epsilon=True):
+    """Harmonic-split mode: every rank holds the whole image,
+    computes the (Q, P) partial sums of its harmonic range, the partial planes
+    are summed over ranks with one NCCL all-reduce over NVLink, and every rank
+    divides.  For single images too small to split by rows.  `src`, `dst`,
+    `workspace`, `bad` are torch CUDA tensors; returns nothing (dst filled)."""
+    import torch
+    import torch.distributed as dist
+    from . import finish_device, partial_sums_device, prepare_device
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    n_lo, n_hi = harmonic_range(approx.N, world, rank)
+    st = torch.cuda.current_stream().cuda_stream
+    pq = torch.zeros((geo.batch, geo.out_rows, geo.width, 2), dtype=torch.float32, device=src.device)
+    prepare_device(src.data_ptr(), geo, spatial, approx, workspace.data_ptr(), workspace.numel(), st, variant,
+                   check_epsilon)
+    if n_hi > n_lo:
+        partial_sums_device(pq.data_ptr(), geo, spatial, approx, n_lo, n_hi, workspace.data_ptr(),
+                            workspace.numel(), st, variant, check_epsilon)
+    if world > 1:
+        dist.all_reduce(pq, op=dist.ReduceOp.SUM, group=group)
+    finish_device(pq.data_ptr(), dst.data_ptr(), geo, spatial, approx, bad.data_ptr(), st, check_epsilon)
+
+
 def geometry(shard: Shard, width: int, height: int):
     """fbf_geometry for a rank's shard (dense per-image buffers)."""
     from . import Geometry, whole_geometry

@@ -75,6 +75,45 @@ def _worker(rank, world, port, img, W, prof, w0, d, eps, q):
     dist.destroy_process_group()
 
 
+def _hsplit_worker(rank, world, port, img, W, prof, d, q):
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.pyoracle import Oracle
+    from paper_1603_08081_b200.shard import harmonic_range
+    n_lo, n_hi = harmonic_range(len(d) - 1, world, rank)
+    P, Q = Oracle().partial_sums(img, prof, W, d, np.pi / 255, n_lo, n_hi)
+    t = torch.from_numpy(np.stack([P, Q]))
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)  # the NCCL all-reduce of the GPU path, on gloo
+    if rank == 0:
+        q.put(t.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_harmonic_split_over_gloo_sums_to_the_whole(oracle, world):
+    """Harmonic-split mode: per-rank partial (P, Q) over disjoint harmonic ranges,
+    summed by an all-reduce, divided -> the whole filter (to rounding)."""
+    rng = np.random.default_rng(9)
+    img = rng.integers(0, 256, (29, 23)).astype(np.float64)
+    W, prof, w0 = oracle.spatial_gaussian(1.5)
+    d, _, eps = oracle.fit_fixed(0, 25.0, 255, 13)
+    whole, rc, _ = oracle.bilateral_fast(img, prof, W, w0, d, np.pi / 255, eps)
+    assert rc == 0
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_hsplit_worker, args=(r, world, port, img, W, prof, d, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    PQ = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert np.allclose(PQ[0] / PQ[1], whole, rtol=0, atol=1e-10)
+
+
 @pytest.mark.parametrize("world", [2])
 def test_strips_over_gloo_reassemble_bit_identically(oracle, world):
     rng = np.random.default_rng(7)
