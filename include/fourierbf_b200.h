@@ -126,6 +126,13 @@ int fbf_convolve_device(int width, int height, const double* profile, int radius
 int fbf_convolve_host_f64(int width, int height, const double* profile, int radius,
                           const double* src, double* dst);
 
+/* bilateral_exact (bilateral.hpp:78-102) on the device in fp64: the O(W^2)
+ * brute-force filter, for checking the paper's bound at full image sizes.
+ * src: fp32 rows [src_row0, src_row0+src_rows) (dense, pitch = width);
+ * dst: fp64 rows [out_row0, out_row0+out_rows); batch must be 1. */
+int fbf_bilateral_exact_device(const fbf_geometry* g, const double* profile, int radius, int family,
+                               double sigma_r, const float* src, double* dst, void* stream);
+
 /* Host-side pieces of the path (stay on the CPU, as in the reference). */
 int fbf_spatial_gaussian(double sigma_s, double* profile, int* radius, double* w0);
 int fbf_spatial_box(int radius, double* profile, double* w0);

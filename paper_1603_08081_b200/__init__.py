@@ -86,6 +86,8 @@ SIGNATURES = {
                                        ctypes.c_double, ctypes.c_int, ctypes.c_int, _F, ctypes.c_int]),
     "fbf_probe_fma_peak": (ctypes.c_int, [_D, _D, _P]),
     "fbf_release_host_buffers": (None, []),
+    "fbf_bilateral_exact_device": (ctypes.c_int, [ctypes.POINTER(Geometry), _D, ctypes.c_int, ctypes.c_int,
+                                                  ctypes.c_double, _P, _P, _P]),
 }
 
 
@@ -309,6 +311,27 @@ def finish_device(pq_ptr: int, dst_ptr: int, geometry: Geometry, spatial: Spatia
 
 def workspace_bytes(geometry: Geometry, radius: int, variant: str = "fused") -> int:
     return int(lib.fbf_workspace_bytes(ctypes.byref(geometry), int(radius), _VARIANTS[variant]))
+
+
+def bilateral_exact_gpu(image: np.ndarray, spatial: SpatialKernel, family: int, sigma_r: float,
+                        row0: int = 0, rows: Optional[int] = None) -> np.ndarray:
+    """bilateral.hpp:78-102 on the GPU (fp64 accumulation): output rows [row0, row0+rows)."""
+    import torch
+    img = np.ascontiguousarray(image, dtype=np.float32)
+    h, w = img.shape
+    rows = h - row0 if rows is None else rows
+    from .shard import source_rows
+    lo, hi = source_rows(row0, rows, h, spatial.radius)
+    g = strip_geometry(w, h, row0, rows, spatial.radius)
+    g.src_row0, g.src_rows = lo, hi - lo
+    dev = torch.device("cuda", torch.cuda.current_device())
+    src = torch.from_numpy(img[lo:hi]).to(dev)
+    dst = torch.empty((rows, w), dtype=torch.float64, device=dev)
+    prof = np.ascontiguousarray(spatial.profile, dtype=np.float64)
+    rc = lib.fbf_bilateral_exact_device(ctypes.byref(g), _dp(prof), spatial.radius, int(family), float(sigma_r),
+                                        src.data_ptr(), dst.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    _check(rc)
+    return dst.cpu().numpy()
 
 
 def convolve(plane: np.ndarray, spatial: SpatialKernel) -> np.ndarray:
