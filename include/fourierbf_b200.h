@@ -133,6 +133,10 @@ int fbf_convolve_host_f64(int width, int height, const double* profile, int radi
 int fbf_bilateral_exact_device(const fbf_geometry* g, const double* profile, int radius, int family,
                                double sigma_r, const float* src, double* dst, void* stream);
 
+/* local_dynamic_range (bilateral.hpp:21-74) on the device, fp64 (exact):
+ * *T = ceil(max over pixels of windowed max - windowed min). */
+int fbf_local_dynamic_range_host_f64(const double* img, int width, int height, int W, int* T);
+
 /* Host-side pieces of the path (stay on the CPU, as in the reference). */
 int fbf_spatial_gaussian(double sigma_s, double* profile, int* radius, double* w0);
 int fbf_spatial_box(int radius, double* profile, double* w0);

@@ -86,6 +86,7 @@ SIGNATURES = {
                                        ctypes.c_double, ctypes.c_int, ctypes.c_int, _F, ctypes.c_int]),
     "fbf_probe_fma_peak": (ctypes.c_int, [_D, _D, _P]),
     "fbf_release_host_buffers": (None, []),
+    "fbf_local_dynamic_range_host_f64": (ctypes.c_int, [_D, ctypes.c_int, ctypes.c_int, ctypes.c_int, _I]),
     "fbf_bilateral_exact_device": (ctypes.c_int, [ctypes.POINTER(Geometry), _D, ctypes.c_int, ctypes.c_int,
                                                   ctypes.c_double, _P, _P, _P]),
 }
@@ -189,6 +190,46 @@ def progressive_fit(family: int, sigma_r: float, T: int, epsilon: float) -> Four
     _check(lib.fbf_progressive_fit(family, float(sigma_r), int(T), float(epsilon), _dp(d), ctypes.byref(n),
                                    ctypes.byref(rn), ctypes.byref(mx)))
     return FourierKernelApprox(int(T), float(np.pi / T), n.value, d[: n.value + 1].copy(), rn.value, mx.value)
+
+
+def local_dynamic_range(image: np.ndarray, W: int) -> int:
+    """bilateral.hpp:21-74 on the GPU (fp64, exact)."""
+    a = np.ascontiguousarray(image, dtype=np.float64)
+    if a.size == 0:
+        raise ValueError("local_dynamic_range: empty image")
+    if W < 1:
+        raise ValueError("local_dynamic_range: window radius must be positive")
+    T = ctypes.c_int()
+    rc = lib.fbf_local_dynamic_range_host_f64(_dp(a), a.shape[1], a.shape[0], int(W), ctypes.byref(T))
+    if rc != FBF_OK:
+        raise FilterError("local_dynamic_range: CUDA failure")
+    return T.value
+
+
+def filter(image: np.ndarray, spatial: SpatialKernel, family: int, sigma_r: float, epsilon: float = 1e-3,
+           integer_intensities: bool = True):
+    """bilateral.hpp:173-196: round, T from the data (GPU), progressive fit (host), bilateral_fast (GPU).
+
+    Returns (output, report dict) like the reference's (Image, AccuracyReport)."""
+    if not epsilon > 0.0:
+        raise ValueError("filter: tolerance must be positive")
+    if not epsilon < spatial.w0:
+        raise ValueError("filter: tolerance must stay below the center spatial weight w(0); lower "
+                         "--epsilon or reduce the spatial radius")
+    src = np.asarray(image, dtype=np.float64)
+    working = np.floor(src + 0.5) if integer_intensities else src
+    T = local_dynamic_range(working, spatial.radius)
+    weaker = not integer_intensities
+    if T == 0:
+        return src.copy(), {"T": 0, "N": None, "epsilon_requested": epsilon, "epsilon_achieved": 0.0,
+                            "w0": spatial.w0, "predicted_bound": 0.0, "weaker_guarantee_flag": weaker}
+    approx = progressive_fit(family, sigma_r, T, epsilon)
+    out = bilateral_fast(working, spatial, approx)
+    bound = (lib.fbf_error_bound(T, approx.max_pointwise_error, spatial.w0)
+             if approx.max_pointwise_error < spatial.w0 else float("inf"))
+    return out, {"T": T, "N": approx.N, "epsilon_requested": epsilon,
+                 "epsilon_achieved": approx.max_pointwise_error, "w0": spatial.w0, "predicted_bound": bound,
+                 "weaker_guarantee_flag": weaker}
 
 
 def error_bound(T: int, epsilon: float, w0: float) -> float:

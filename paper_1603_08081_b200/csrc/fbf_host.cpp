@@ -394,40 +394,15 @@ AccuracyReport make_report(int T, double epsilon_requested, double epsilon_achie
 
 // -------------------------------------------------------------- bilateral.hpp
 
-namespace {
-
-// windowed extreme over [-W, W] along one axis with mirror padding (exact)
-void window_extreme_1d(const std::vector<double>& in, std::vector<double>& out, int w, int h,
-                       int W, bool along_x, bool take_max) {
-    for (int y = 0; y < h; ++y)
-        for (int x = 0; x < w; ++x) {
-            double e = take_max ? -std::numeric_limits<double>::infinity()
-                                : std::numeric_limits<double>::infinity();
-            for (int k = -W; k <= W; ++k) {
-                const int sx = along_x ? mirror_index(x + k, w) : x;
-                const int sy = along_x ? y : mirror_index(y + k, h);
-                const double v = in[static_cast<std::size_t>(sy) * w + sx];
-                e = take_max ? std::max(e, v) : std::min(e, v);
-            }
-            out[static_cast<std::size_t>(y) * w + x] = e;
-        }
-}
-
-}  // namespace
-
 int local_dynamic_range(const Image& image, int W) {
     if (image.width <= 0 || image.height <= 0)
         throw std::invalid_argument("local_dynamic_range: empty image");
     if (W < 1) throw std::invalid_argument("local_dynamic_range: window radius must be positive");
-    const int w = image.width, h = image.height;
-    std::vector<double> t(image.values.size()), hi(image.values.size()), lo(image.values.size());
-    window_extreme_1d(image.values, t, w, h, W, true, true);
-    window_extreme_1d(t, hi, w, h, W, false, true);
-    window_extreme_1d(image.values, t, w, h, W, true, false);
-    window_extreme_1d(t, lo, w, h, W, false, false);
-    double spread = 0.0;
-    for (std::size_t i = 0; i < hi.size(); ++i) spread = std::max(spread, hi[i] - lo[i]);
-    return static_cast<int>(std::ceil(spread));
+    // on the device (fbf_ldr.cu): filter()'s T, exact in fp64
+    int T = 0;
+    const int rc = fbf_local_dynamic_range_host_f64(image.values.data(), image.width, image.height, W, &T);
+    if (rc != FBF_OK) throw std::runtime_error("local_dynamic_range: CUDA failure");
+    return T;
 }
 
 Image bilateral_exact(const Image& image, const SpatialKernel& spatial, const RangeKernel& range) {

@@ -115,13 +115,39 @@ static void host_checks() {
   bad.max_pointwise_error = 0.5;
   CHECK(throws<std::invalid_argument>(
       [&] { bilateral_fast(random_integer_image(8, 8, 7), make_spatial_gaussian(3.0), bad); }));
-  CHECK(local_dynamic_range(Image(5, 4, 9.0), 2) == 0);
-  Image two(2, 2);
-  two(1, 0) = two(1, 1) = 255.0;
-  CHECK(local_dynamic_range(two, 1) == 255);
+  CHECK(throws<std::invalid_argument>([] { local_dynamic_range(Image(), 1); }));
+  CHECK(throws<std::invalid_argument>([] { local_dynamic_range(Image(4, 4, 0.0), 0); }));
 }
 
 static void gpu_checks() {
+  // test_bilateral.cpp:133-162 local_dynamic_range (now on the device, fp64)
+  {
+    CHECK(local_dynamic_range(Image(5, 4, 9.0), 2) == 0);
+    Image two(2, 2);
+    two(1, 0) = two(1, 1) = 255.0;
+    CHECK(local_dynamic_range(two, 1) == 255);
+    Image frac(3, 1, 0.0);
+    frac(1, 0) = 1.25;
+    CHECK(local_dynamic_range(frac, 1) == 2);
+    for (unsigned seed = 0; seed < 6; ++seed) {
+      const Image img = random_integer_image(seed % 2 ? 7 : 16, seed % 3 ? 5 : 12, seed);
+      for (const int W : {1, 2, 5}) {
+        double spread = 0.0;  // brute force, test_bilateral.cpp:68-83
+        for (int y = 0; y < img.height; ++y)
+          for (int x = 0; x < img.width; ++x) {
+            double hi = -1e300, lo = 1e300;
+            for (int jy = -W; jy <= W; ++jy)
+              for (int jx = -W; jx <= W; ++jx) {
+                const double v = img(mirror_index(x - jx, img.width), mirror_index(y - jy, img.height));
+                hi = std::max(hi, v);
+                lo = std::min(lo, v);
+              }
+            spread = std::max(spread, hi - lo);
+          }
+        CHECK(local_dynamic_range(img, W) == static_cast<int>(std::ceil(spread)));
+      }
+    }
+  }
   // test_bilateral.cpp:218-224 constant pass-through
   {
     const Image img(8, 8, 120.0);
