@@ -18,7 +18,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libfourierbf_b200.so")
+# FBF_LIBRARY: diagnostics only (tools/phase_probe.py loads an instrumented build)
+LIB_PATH = os.environ.get("FBF_LIBRARY") or os.path.join(_HERE, "_lib", "libfourierbf_b200.so")
 
 FBF_OK, FBF_EINVAL, FBF_EANOMALY, FBF_ECUDA, FBF_EUNSUPPORTED = 0, 1, 2, 3, 4
 SPATIAL_GAUSSIAN, SPATIAL_BOX = 0, 1

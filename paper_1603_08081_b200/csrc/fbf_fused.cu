@@ -33,7 +33,19 @@ bool fused_supported(int W, bool box) {
   }
 }
 
-cudaError_t launch_fused(const FusedArgs& a, cudaStream_t st, int* grid_out) {
+#ifdef FBF_PHASE_PROF
+static unsigned long long* g_prof = nullptr;
+#endif
+
+cudaError_t launch_fused(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
+  FusedArgs a = a_in;
+#ifdef FBF_PHASE_PROF
+  if (!g_prof) {
+    cudaMalloc(&g_prof, 32 * sizeof(unsigned long long));
+    cudaMemset(g_prof, 0, 32 * sizeof(unsigned long long));
+  }
+  a.prof = g_prof;
+#endif
   if (a.k.box) {
     switch (a.k.W) {
       case 2: return launch_w<2, true>(a, st, grid_out);
@@ -57,3 +69,14 @@ cudaError_t launch_fused(const FusedArgs& a, cudaStream_t st, int* grid_out) {
 }
 
 }  // namespace fbf
+
+#ifdef FBF_PHASE_PROF
+// diagnostics: summed per-phase cycles of thread 0 of every CTA (see fbf_fused.cuh)
+extern "C" int fbf_debug_phase_prof(unsigned long long* out32) {
+  if (!fbf::g_prof) return -1;
+  cudaDeviceSynchronize();
+  cudaMemcpy(out32, fbf::g_prof, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaMemset(fbf::g_prof, 0, 32 * sizeof(unsigned long long));
+  return 0;
+}
+#endif

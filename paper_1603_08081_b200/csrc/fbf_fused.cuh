@@ -37,29 +37,40 @@ namespace fbf {
 // BOX: uniform window -> O(1) running sums (2 adds per output per pass in the
 // steady state) instead of the (2W+1)-tap FIR; the 1/(2W+1)^2 weight is applied
 // once, in the demodulation.
+//
+// Channel halves: the four real planes of a harmonic travel as two pairs,
+// half A = (c, f'c) and half B = (s, f's), stored as separate 8-byte planes.
+// Lanes 0-15 of a warp filter half A and lanes 16-31 the same pixels' half B,
+// each with KR (KC) = 16 outputs per lane: per output a lane loads
+// (16+2W)/16 8-byte words instead of (8+2W)/8 16-byte words, which cuts the
+// shared-memory traffic of the two FIR passes by ~40% (the FIR loads were
+// half of all smem wavefronts; profiles/r01_notes.md).  The two halves of an
+// output meet in the demodulation through one shuffle (lane ^ 16).
 template <int W_, int TW_, int G_, int KR_, int KC_, int NT_, bool BOX_ = false>
 struct FusedCfg {
   static constexpr int W = W_, TW = TW_, G = G_, KR = KR_, KC = KC_, NT = NT_;
   static constexpr bool BOX = BOX_;
   static constexpr int MW = TW + 2 * W;   // modulated row width
-  static constexpr int MP = MW | 1;       // M pitch in 16-byte units (odd: conflict-free column walks)
+  static constexpr int MP = MW | 1;       // M plane pitch in 8-byte units (odd: conflict-free row walks)
   static constexpr int RING = 2 * W + G;  // R ring rows
   static constexpr int CRING = W + G;     // CS ring rows
-  static constexpr int RP = TW + 1;       // R pitch in 16-byte units
+  static constexpr int RP = TW + 1;       // R plane pitch in 8-byte units
   static constexpr int CP = TW + 1;       // CS pitch in 8-byte units
   static constexpr int PROLOGUE = (2 * W + G - 1) / G;  // steps that only row-pass
+  static constexpr int HALF = 16;         // lanes per channel half
   // smem carve-up (bytes; TMA destinations 128-byte aligned)
   static constexpr size_t up128(size_t v) { return (v + 127) & ~size_t(127); }
   static constexpr size_t OFF_STAGE = 0;
   static constexpr size_t OFF_PQ = up128(OFF_STAGE + size_t(G) * MW * 8);
-  static constexpr size_t OFF_M = up128(OFF_PQ + size_t(G) * TW * 8);
-  static constexpr size_t OFF_R = OFF_M + size_t(G) * MP * 16;
-  static constexpr size_t OFF_CS = OFF_R + size_t(RING) * RP * 16;
+  static constexpr size_t OFF_M = up128(OFF_PQ + size_t(G) * TW * 8);  // planes A, B
+  static constexpr size_t OFF_R = OFF_M + 2 * size_t(G) * MP * 8;      // planes A, B
+  static constexpr size_t OFF_CS = OFF_R + 2 * size_t(RING) * RP * 8;
   static constexpr size_t OFF_BAR = up128(OFF_CS + size_t(CRING) * CP * 8);
   static constexpr size_t smem_bytes = OFF_BAR + 16;
-  static_assert(G * (TW / KR) == NT, "row pass: one (row, chunk) item per thread");
-  static_assert((G / KC) * TW == NT, "column pass: one (column, run) item per thread");
-  static_assert(TW % KR == 0 && G % KC == 0, "tiling");
+  static_assert(KR == 16 && KC == 16, "one lane per (half, 16 outputs)");
+  static_assert(G % HALF == 0 && TW % HALF == 0, "tiling");
+  static_assert((G / HALF) * (TW / KR) * 32 == NT, "row pass: one (16 rows, chunk) item per warp");
+  static_assert((TW / HALF) * (G / KC) * 32 == NT, "column pass: one (16 columns, run) item per warp");
   static_assert(smem_bytes <= 227 * 1024, "shared memory budget");
 };
 
@@ -118,7 +129,7 @@ template <class C>
 struct ModNext {
   static constexpr int ELEMS = Lanes<C>::RPW * Lanes<C>::NJ;
   const int2* stage;
-  ulonglong2* M;
+  p2* M;  // plane A; plane B follows at + G * MP
   uint32_t n;
 
   // k must be a constant after unrolling (all callers sit in unrolled loops)
@@ -134,13 +145,15 @@ struct ModNext {
     float c, s;
     sincos_turns(n * static_cast<uint32_t>(v.x), c, s);
     const float fp = __int_as_float(v.y);
-    const ulonglong2 m = make_ulonglong2(pk(c, c * fp), pk(s, s * fp));
-    if (full || j < C::MW) M[g * C::MP + j] = m;
+    if (full || j < C::MW) {
+      M[g * C::MP + j] = pk(c, c * fp);
+      M[(C::G + g) * C::MP + j] = pk(s, s * fp);
+    }
   }
 };
 
 template <class C>
-__device__ __forceinline__ void modulate_rows(const int2* __restrict__ stage, ulonglong2* __restrict__ M,
+__device__ __forceinline__ void modulate_rows(const int2* __restrict__ stage, p2* __restrict__ M,
                                               int rows, uint32_t n) {
   (void)rows;
   const ModNext<C> job{stage, M, n};
@@ -148,75 +161,112 @@ __device__ __forceinline__ void modulate_rows(const int2* __restrict__ stage, ul
   for (int k = 0; k < ModNext<C>::ELEMS; ++k) job.element(k);
 }
 
+// FBF_PHASE_PROF builds: thread 0 of every CTA sums the cycles of each phase
+// of the step loop into A.prof (diagnostics, tools/phase_probe.py); otherwise
+// the marks compile to nothing.
+struct PhaseClock {
+#ifdef FBF_PHASE_PROF
+  unsigned long long ph[9];  // 8 phases + step count
+  long long t;
+  __device__ __forceinline__ void start() {
+    for (int i = 0; i < 9; ++i) ph[i] = 0;
+    t = clock64();
+  }
+  __device__ __forceinline__ void mark(int i) {
+    if (threadIdx.x == 0) {
+      const long long now = clock64();
+      ph[i] += now - t;
+      t = now;
+    }
+  }
+  __device__ __forceinline__ void flush(unsigned long long* out) {
+    if (threadIdx.x == 0 && out)
+      for (int i = 0; i < 9; ++i) atomicAdd(out + i, ph[i]);
+  }
+  __device__ __forceinline__ void step() { ph[8] += threadIdx.x == 0; }
+#else
+  __device__ __forceinline__ void step() {}
+  __device__ __forceinline__ void start() {}
+  __device__ __forceinline__ void mark(int) {}
+  __device__ __forceinline__ void flush(unsigned long long*) {}
+#endif
+};
+
+// Row pass: warp = (16 rows, one KR-chunk of output columns); lane l filters
+// row g of half h = l / 16 (plane A or B) into the R ring, and stores its
+// half of the centre (c, s) of each input row's KR pixels into the CS ring.
 template <class C>
-__device__ __forceinline__ void row_pass(const FusedArgs& A, const ulonglong2* __restrict__ M,
-                                         ulonglong2* __restrict__ R, p2* __restrict__ CS, int a,
-                                         int rows, int base) {
-  const int g = threadIdx.x % C::G;
-  const int xc = (threadIdx.x / C::G) * C::KR;
+__device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restrict__ M, p2* __restrict__ R,
+                                         float* __restrict__ CS, int a, int rows, int base) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int h = lane >> 4;
+  const int g = (lane & 15) + C::HALF * (warp % (C::G / C::HALF));
+  const int xc = (warp / (C::G / C::HALF)) * C::KR;
   if (g >= rows) return;
-  const ulonglong2* __restrict__ src = M + g * C::MP + xc;
+  const p2* __restrict__ src = M + (h * C::G + g) * C::MP + xc;
   const int rel = a + g - base;
   const int slot = rel % C::RING;
-  const int cslot = rel % C::CRING;
-  p2 accA[C::KR], accB[C::KR];
+  float* __restrict__ csrow = CS + 2 * (rel % C::CRING) * C::CP + h;
+  p2 acc[C::KR];
   if constexpr (C::BOX) {
     // running sum over the window [i, i+2W] (unweighted)
-    p2 sA = 0ull, sB = 0ull;
+    p2 sum = 0ull;
 #pragma unroll
     for (int m = 0; m <= 2 * C::W; ++m) {
-      const ulonglong2 v = src[m];
-      sA = add2(sA, v.x);
-      sB = add2(sB, v.y);
-      if (m >= C::W && m < C::W + C::KR) CS[cslot * C::CP + xc + (m - C::W)] = pk(lo_of(v.x), lo_of(v.y));
+      const p2 v = src[m];
+      sum = add2(sum, v);
+      if (m >= C::W && m < C::W + C::KR) csrow[2 * (xc + m - C::W)] = lo_of(v);
     }
-    accA[0] = sA;
-    accB[0] = sB;
+    acc[0] = sum;
 #pragma unroll
     for (int i = 1; i < C::KR; ++i) {
-      const ulonglong2 vin = src[i + 2 * C::W], vout = src[i - 1];
-      sA = sub2(add2(sA, vin.x), vout.x);
-      sB = sub2(add2(sB, vin.y), vout.y);
-      accA[i] = sA;
-      accB[i] = sB;
-      if (i + 2 * C::W >= C::W && i + 2 * C::W < C::W + C::KR)
-        CS[cslot * C::CP + xc + (i + C::W)] = pk(lo_of(vin.x), lo_of(vin.y));
+      const p2 vin = src[i + 2 * C::W], vout = src[i - 1];
+      sum = sub2(add2(sum, vin), vout);
+      acc[i] = sum;
+      const int m = i + 2 * C::W;
+      if (m >= C::W && m < C::W + C::KR) csrow[2 * (xc + m - C::W)] = lo_of(vin);
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < C::KR; ++i) accA[i] = accB[i] = 0ull;
+    for (int i = 0; i < C::KR; ++i) acc[i] = 0ull;
 #pragma unroll
     for (int m = 0; m < C::KR + 2 * C::W; ++m) {
-      const ulonglong2 v = src[m];
+      const p2 v = src[m];
 #pragma unroll
       for (int i = 0; i < C::KR; ++i) {
         const int j = m - i;
         if (j >= 0 && j <= 2 * C::W) {
           const float tv = A.k.t[j < C::W ? C::W - j : j - C::W];
-          accA[i] = fma2(pk(tv, tv), v.x, accA[i]);
-          accB[i] = fma2(pk(tv, tv), v.y, accB[i]);
+          acc[i] = fma2(pk(tv, tv), v, acc[i]);
         }
       }
-      if (m >= C::W && m < C::W + C::KR)  // centre (c, s) of output column xc + m - W
-        CS[cslot * C::CP + xc + (m - C::W)] = pk(lo_of(v.x), lo_of(v.y));
+      if (m >= C::W && m < C::W + C::KR)  // centre of output column xc + m - W
+        csrow[2 * (xc + m - C::W)] = lo_of(v);
     }
   }
-  ulonglong2* __restrict__ dst = R + slot * C::RP + xc;
+  p2* __restrict__ dst = R + (h * C::RING + slot) * C::RP + xc;
 #pragma unroll
-  for (int i = 0; i < C::KR; ++i) dst[i] = make_ulonglong2(accA[i], accB[i]);
+  for (int i = 0; i < C::KR; ++i) dst[i] = acc[i];
 }
 
+// Column pass: warp = (16 columns, one KC-run of output rows); lane l filters
+// half h = l / 16 of column x.  Demodulation: each lane forms c*acc (half A)
+// or s*acc (half B) for its KC rows, the two halves swap the partials of each
+// other's 8 output rows with one shuffle, and each lane finishes 8 rows.
 template <class C>
-__device__ __forceinline__ void col_pass(const FusedArgs& A, const ulonglong2* __restrict__ R,
-                                         const p2* __restrict__ CS, const p2* __restrict__ pqs,
+__device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restrict__ R,
+                                         const float* __restrict__ CS, const p2* __restrict__ pqs,
                                          const Unit& u, int o, int base, int n, bool first, bool divide,
-                                         const ModNext<C>& next) {
-  const int x = threadIdx.x % C::TW;
-  const int gi = (threadIdx.x / C::TW) * C::KC;  // first output row of this thread, rel. to o
+                                         const ModNext<C>& next, PhaseClock& clk) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int h = lane >> 4;
+  const int x = (lane & 15) + C::HALF * (warp % (C::TW / C::HALF));
+  const int gi = (warp / (C::TW / C::HALF)) * C::KC;  // first output row of this lane, rel. to o
   const int r0 = o + gi;
   const int gx = u.x0 + x;
-  const int nr = min(C::KC, u.y1 - r0);  // <= 0: this thread only helps with the modulation
-  p2 accA[C::KC], accB[C::KC];
+  const int nr = min(C::KC, u.y1 - r0);  // <= 0: this lane only helps with the modulation
+  p2 acc[C::KC];
+  const p2* __restrict__ Rh = R + h * C::RING * C::RP + x;
   const int s0 = (r0 - C::W - base) % C::RING;
   constexpr int TAPS_IN = C::KC + 2 * C::W;
   constexpr int ELEMS = ModNext<C>::ELEMS;
@@ -224,42 +274,35 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const ulonglong2* _
   auto ring = [&](int m) {
     int s = s0 + m;
     s = s >= C::RING ? s - C::RING : s;
-    return R[s * C::RP + x];
+    return Rh[s * C::RP];
   };
   if constexpr (C::BOX) {
-    p2 sA = 0ull, sB = 0ull;
+    p2 sum = 0ull;
 #pragma unroll
     for (int m = 0; m <= 2 * C::W; ++m) {
-      const ulonglong2 v = ring(m);
-      sA = add2(sA, v.x);
-      sB = add2(sB, v.y);
+      sum = add2(sum, ring(m));
       if (m % STRIDE == 0 && m / STRIDE < ELEMS) next.element(m / STRIDE);
     }
-    accA[0] = sA;
-    accB[0] = sB;
+    acc[0] = sum;
 #pragma unroll
     for (int i = 1; i < C::KC; ++i) {
-      const ulonglong2 vin = ring(i + 2 * C::W), vout = ring(i - 1);
-      sA = sub2(add2(sA, vin.x), vout.x);
-      sB = sub2(add2(sB, vin.y), vout.y);
-      accA[i] = sA;
-      accB[i] = sB;
+      sum = sub2(add2(sum, ring(i + 2 * C::W)), ring(i - 1));
+      acc[i] = sum;
       const int m = i + 2 * C::W;
       if (m % STRIDE == 0 && m / STRIDE < ELEMS) next.element(m / STRIDE);
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < C::KC; ++i) accA[i] = accB[i] = 0ull;
+    for (int i = 0; i < C::KC; ++i) acc[i] = 0ull;
 #pragma unroll
     for (int m = 0; m < TAPS_IN; ++m) {
-      const ulonglong2 v = ring(m);
+      const p2 v = ring(m);
 #pragma unroll
       for (int i = 0; i < C::KC; ++i) {
         const int j = m - i;
         if (j >= 0 && j <= 2 * C::W) {
           const float tv = A.k.t[j < C::W ? C::W - j : j - C::W];
-          accA[i] = fma2(pk(tv, tv), v.x, accA[i]);
-          accB[i] = fma2(pk(tv, tv), v.y, accB[i]);
+          acc[i] = fma2(pk(tv, tv), v, acc[i]);
         }
       }
       // one slice of the next step's modulation per STRIDE taps
@@ -268,54 +311,66 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const ulonglong2* _
   }
 #pragma unroll
   for (int k = TAPS_IN / STRIDE + (TAPS_IN % STRIDE ? 1 : 0); k < ELEMS; ++k) next.element(k);
-  if (nr <= 0 || gx >= A.g.width) return;
-  // box: both passes summed unweighted; the weight (1/(2W+1))^2 = w0 joins d_n here
-  const float dn = C::BOX ? A.h.d[n] * (A.k.box_tap * A.k.box_tap) : A.h.d[n];
-  const p2 dd = pk(dn, dn);
+  clk.mark(5);
+  // (q, p) = c (Gc, Fc) + s (Gs, Fs)   [bilateral.hpp:138-144, real form]:
+  // this lane's half of every row, then swap halves with the partner lane
+  constexpr int KH = C::KC / 2;
   const int cs0 = (r0 - base) % C::CRING;
-  p2* __restrict__ pqrow = reinterpret_cast<p2*>(A.pq) +
-                           ((blockIdx.y * A.g.batch + u.b) * static_cast<long long>(A.g.out_rows) +
-                            (r0 - A.g.out_row0)) * A.pq_cols + gx;
-  const int wstride = A.pq_cols;
-  // demodulate all KC outputs straight-line; only the global stores are predicated
-  p2 qp[C::KC];
+  p2 part[C::KC];
 #pragma unroll
   for (int i = 0; i < C::KC; ++i) {
     int sc = cs0 + i;
     sc = sc >= C::CRING ? sc - C::CRING : sc;
-    float c, s;
-    upk(CS[sc * C::CP + x], c, s);
-    // (q, p) = c (Gc, Fc) + s (Gs, Fs)   [bilateral.hpp:138-144, real form]
-    qp[i] = fma2(pk(s, s), accB[i], mul2(pk(c, c), accA[i]));
+    const float w = CS[2 * (sc * C::CP + x) + h];
+    part[i] = mul2(pk(w, w), acc[i]);
   }
+  p2 qp[KH];
+#pragma unroll
+  for (int k = 0; k < KH; ++k) {
+    const p2 send = h ? part[k] : part[KH + k];
+    const p2 own = h ? part[KH + k] : part[k];
+    qp[k] = add2(own, __shfl_xor_sync(0xffffffffu, send, 16));
+  }
+  if (gx >= A.g.width) return;
+  const int rr = r0 + h * KH;  // first output row of this lane
+  const int nh = nr - h * KH;  // rows of this lane (may be <= 0)
+  if (nh <= 0) return;
+  // box: both passes summed unweighted; the weight (1/(2W+1))^2 = w0 joins d_n here
+  const float dn = C::BOX ? A.h.d[n] * (A.k.box_tap * A.k.box_tap) : A.h.d[n];
+  const p2 dd = pk(dn, dn);
+  const p2* __restrict__ pqin = pqs + (gi + h * KH) * C::TW + x;
   if (!divide) {
+    p2* __restrict__ pqrow = reinterpret_cast<p2*>(A.pq) +
+                             ((blockIdx.y * A.g.batch + u.b) * static_cast<long long>(A.g.out_rows) +
+                              (rr - A.g.out_row0)) * A.pq_cols + gx;
+    const int wstride = A.pq_cols;
     if (first) {
 #pragma unroll
-      for (int i = 0; i < C::KC; ++i)
-        if (i < nr) pqrow[i * wstride] = mul2(dd, qp[i]);
+      for (int k = 0; k < KH; ++k)
+        if (k < nh) pqrow[k * wstride] = mul2(dd, qp[k]);
     } else {
 #pragma unroll
-      for (int i = 0; i < C::KC; ++i)
-        if (i < nr) pqrow[i * wstride] = fma2(dd, qp[i], pqs[(gi + i) * C::TW + x]);
+      for (int k = 0; k < KH; ++k)
+        if (k < nh) pqrow[k * wstride] = fma2(dd, qp[k], pqin[k * C::TW]);
     }
     return;
   }
   // bilateral.hpp:147-158: divide; flag the first collapsed denominator
   float* __restrict__ drow = A.dst + u.b * A.g.dst_bstride +
-                             static_cast<long long>(r0 - A.g.out_row0) * A.g.dst_pitch + gx;
+                             static_cast<long long>(rr - A.g.out_row0) * A.g.dst_pitch + gx;
 #pragma unroll
-  for (int i = 0; i < C::KC; ++i) {
-    if (i < nr) {
-      const p2 acc = first ? mul2(dd, qp[i]) : fma2(dd, qp[i], pqs[(gi + i) * C::TW + x]);
+  for (int k = 0; k < KH; ++k) {
+    if (k < nh) {
+      const p2 acc2 = first ? mul2(dd, qp[k]) : fma2(dd, qp[k], pqin[k * C::TW]);
       float Q, P;
-      upk(acc, Q, P);
+      upk(acc2, Q, P);
       if (!(fabsf(Q) >= A.h.q_floor) && A.bad) {
         const unsigned long long lin =
             static_cast<unsigned long long>(u.b) * A.g.full_height * A.g.width +
-            static_cast<unsigned long long>(r0 + i) * A.g.width + gx;
+            static_cast<unsigned long long>(rr + k) * A.g.width + gx;
         atomicMin(A.bad, lin);
       }
-      drow[i * static_cast<long long>(A.g.dst_pitch)] = A.h.shift + __fdiv_rn(P, Q);
+      drow[k * static_cast<long long>(A.g.dst_pitch)] = A.h.shift + __fdiv_rn(P, Q);
     }
   }
 }
@@ -324,9 +379,9 @@ template <class C>
 __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(const __grid_constant__ FusedArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   int2* stage = reinterpret_cast<int2*>(smem + C::OFF_STAGE);
-  ulonglong2* M = reinterpret_cast<ulonglong2*>(smem + C::OFF_M);
-  ulonglong2* R = reinterpret_cast<ulonglong2*>(smem + C::OFF_R);
-  p2* CS = reinterpret_cast<p2*>(smem + C::OFF_CS);
+  p2* M = reinterpret_cast<p2*>(smem + C::OFF_M);
+  p2* R = reinterpret_cast<p2*>(smem + C::OFF_R);
+  float* CS = reinterpret_cast<float*>(smem + C::OFF_CS);
   p2* pqs = reinterpret_cast<p2*>(smem + C::OFF_PQ);
   uint64_t* bar_uf = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* bar_pq = bar_uf + 1;
@@ -338,6 +393,9 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
   }
   __syncthreads();
   unsigned ph_uf = 0, ph_pq = 0;  // phase parity of the next completion of each barrier
+  PhaseClock clk;
+  clk.start();
+
   // this CTA group's harmonics [nb, ne)
   const int span = A.n_hi - A.n_lo;
   const int nb = A.n_lo + span * static_cast<int>(blockIdx.y) / A.groups;
@@ -391,13 +449,16 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
         const bool more = !wrap || n + 1 < ne;
         const bool want_pq = o >= 0 && !first;
         step_rows<C>(u, wrap ? 0 : s + 1, a2, rows2, o2);
+        clk.mark(0);
         __syncthreads();  // S1: M holds this step; the previous column pass is done; stage free
+        clk.mark(1);
         if (leader) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           if (more) tma_uf<C>(A, stage, bar_uf, u, a2);
           if (want_pq) tma_pq<C>(A, pqs, bar_pq, u, o);
         }
         row_pass<C>(A, M, R, CS, a, rows, base);
+        clk.mark(2);
         if (more) {
           mbar_wait(bar_uf, ph_uf);
           ph_uf ^= 1u;
@@ -406,18 +467,25 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
           mbar_wait(bar_pq, ph_pq);
           ph_pq ^= 1u;
         }
+        clk.mark(3);
         __syncthreads();  // S2: ring rows visible, next (u, f') and this step's (Q, P) landed, M free
+        clk.mark(4);
         // the next step's modulation is interleaved into this step's column pass
         // (its ALU work issues in the FFMA2 shadow); prologue steps run it alone
         const ModNext<C> next{stage, M, static_cast<uint32_t>(wrap ? n + 1 : n)};
-        if (o >= 0)
-          col_pass<C>(A, R, CS, pqs, u, o, base, n, first, divide, next);
-        else
+        if (o >= 0) {
+          col_pass<C>(A, R, CS, pqs, u, o, base, n, first, divide, next, clk);
+          clk.mark(7);
+        } else {
           modulate_rows<C>(stage, M, rows2, next.n);
+          clk.mark(6);
+        }
+        clk.step();
       }
     }
     pos += len;
   }
+  clk.flush(A.prof);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -486,8 +554,8 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
 // FBF_FUSED_CFG=small|big overrides where both fit (experiments).
 template <int W, bool BOX = false>
 cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
-  using Small = FusedCfg<W, 64, 16, 8, 8, 128, BOX>;
-  using Big = FusedCfg<W, 64, 32, 8, 8, 256, BOX>;
+  using Small = FusedCfg<W, 64, 16, 16, 16, 128, BOX>;
+  using Big = FusedCfg<W, 64, 32, 16, 16, 256, BOX>;
   if constexpr (Small::smem_bytes <= 113 * 1024) {
     const char* env = getenv("FBF_FUSED_CFG");
     const bool big = env ? env[0] == 'b' : !(W <= 9);

@@ -72,6 +72,7 @@ struct FusedArgs {
   int strips;              // ceil(width / TW)
   long long total;         // batch * strips * out_rows
   int seg_max;             // longest row run one CTA filters in one pass over n
+  unsigned long long* prof;  // phase cycle counters (FBF_PHASE_PROF builds only), else null
 };
 
 }  // namespace fbf

@@ -19,7 +19,7 @@ from dataclasses import dataclass
 from typing import List
 
 
-ROW_ALIGN = 8  # = the fused kernel's rows per column-pass block (KC)
+ROW_ALIGN = 16  # = the fused kernel's rows per column-pass block (KC)
 
 
 @dataclass(frozen=True)
