@@ -170,4 +170,46 @@ __device__ __forceinline__ void sincos_turns(uint32_t p, float& c_out, float& s_
   s_out = __uint_as_float(sb);
 }
 
+// sincos_turns of NB phases n * v[b].x, each stage issued for all NB (ILP)
+template <int NB>
+__device__ __forceinline__ void sincos_turns_n(uint32_t n, const int2 (&v)[NB], float (&c_out)[NB],
+                                               float (&s_out)[NB]) {
+  uint32_t q[NB];
+  float r[NB];
+  p2 t[NB], zz[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const uint32_t pq = n * static_cast<uint32_t>(v[b].x) + 0x20000000u;
+    q[b] = pq >> 30;
+    const int32_t ri = static_cast<int32_t>(pq & 0x3FFFFFFFu) - 0x20000000;
+    r[b] = static_cast<float>(ri) * 1.4629180792671596e-09f;  // 2 pi / 2^32
+  }
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const float z = r[b] * r[b];
+    zz[b] = pk(z, z);
+    t[b] = fma2(pk(2.716014023462776e-06f, 2.4390450562350452e-05f), zz[b],
+                pk(-1.9839043670799583e-04f, -1.3886763481423259e-03f));
+  }
+#pragma unroll
+  for (int b = 0; b < NB; ++b) t[b] = fma2(t[b], zz[b], pk(8.333328180015087e-03f, 4.166662320494652e-02f));
+#pragma unroll
+  for (int b = 0; b < NB; ++b) t[b] = fma2(t[b], zz[b], pk(-1.666666716337204e-01f, -0.5f));
+#pragma unroll
+  for (int b = 0; b < NB; ++b) t[b] = fma2(t[b], zz[b], pk(1.0f, 1.0f));
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    float ts, tc;
+    upk(t[b], ts, tc);
+    const float sr = r[b] * ts, cr = tc;
+    const bool odd = q[b] & 1u;
+    uint32_t cb = __float_as_uint(odd ? sr : cr);
+    uint32_t sb = __float_as_uint(odd ? cr : sr);
+    cb ^= ((q[b] + 1u) & 2u) << 30;
+    sb ^= (q[b] & 2u) << 30;
+    c_out[b] = __uint_as_float(cb);
+    s_out[b] = __uint_as_float(sb);
+  }
+}
+
 }  // namespace fbf

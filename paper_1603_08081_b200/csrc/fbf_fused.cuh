@@ -133,7 +133,12 @@ struct ModNext {
   uint32_t n;
 
   // k must be a constant after unrolling (all callers sit in unrolled loops)
-  __device__ __forceinline__ void element(int k) const {
+  __device__ __forceinline__ void element(int k) const { element_at(k, stage, M, n); }
+  // restrict-qualified form: callers that interleave the elements with other
+  // shared-memory traffic pass their pointers here, so the compiler may move
+  // the element chains past the other loads and stores
+  static __device__ __forceinline__ void element_at(int k, const int2* __restrict__ stage, p2* __restrict__ M,
+                                                    uint32_t n) {
     using L = Lanes<C>;
     const int r = k / L::NJ, i = k % L::NJ;
     const bool full = (C::MW % 32 == 0) || (i + 1 < L::NJ);
@@ -150,20 +155,57 @@ struct ModNext {
       M[(C::G + g) * C::MP + j] = pk(s, s * fp);
     }
   }
+  // elements K0 .. K0+NB-1 with every stage of the chain issued for all NB
+  // before the next: NB independent chains in flight (the compiler tends to
+  // run single elements back to back, exposing the ~20-deep dependency chain)
+  // (k0 must be a constant after unrolling)
+  template <int NB>
+  static __device__ __forceinline__ void elements(int k0, const int2* __restrict__ stage, p2* __restrict__ M,
+                                                  uint32_t n) {
+    using L = Lanes<C>;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int2 v[NB];
+    int off[NB];
+    bool ok[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int k = k0 + b;
+      const int r = k / L::NJ, i = k % L::NJ;
+      const bool full = (C::MW % 32 == 0) || (i + 1 < L::NJ);
+      const int g = warp + r * L::NWARP;
+      const int j = lane + 32 * i;
+      const int jc = full ? j : min(j, C::MW - 1);
+      ok[b] = full || j < C::MW;
+      off[b] = g * C::MP + j;
+      v[b] = stage[g * C::MW + jc];
+    }
+    float c[NB], s[NB];
+    sincos_turns_n<NB>(n, v, c, s);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const float fp = __int_as_float(v[b].y);
+      if (ok[b]) {
+        M[off[b]] = pk(c[b], c[b] * fp);
+        M[C::G * C::MP + off[b]] = pk(s[b], s[b] * fp);
+      }
+    }
+  }
 };
 
 template <class C>
 __device__ __forceinline__ void modulate_rows(const int2* __restrict__ stage, p2* __restrict__ M,
                                               int rows, uint32_t n) {
   (void)rows;
-  const ModNext<C> job{stage, M, n};
+  constexpr int E = ModNext<C>::ELEMS;
 #pragma unroll
-  for (int k = 0; k < ModNext<C>::ELEMS; ++k) job.element(k);
+  for (int k = 0; k + 4 <= E; k += 4) ModNext<C>::template elements<4>(k, stage, M, n);
+#pragma unroll
+  for (int k = E - E % 4; k < E; ++k) ModNext<C>::element_at(k, stage, M, n);
 }
 
-// FBF_PHASE_PROF builds: thread 0 of every CTA sums the cycles of each phase
-// of the step loop into A.prof (diagnostics, tools/phase_probe.py); otherwise
-// the marks compile to nothing.
+// FBF_PHASE_PROF builds: thread 0 (and 128) of every CTA sums the cycles of
+// each phase of the step loop into A.prof (diagnostics, tools/phase_probe.py);
+// otherwise the marks compile to nothing.
 struct PhaseClock {
 #ifdef FBF_PHASE_PROF
   unsigned long long ph[9];  // 8 phases + step count
@@ -173,17 +215,17 @@ struct PhaseClock {
     t = clock64();
   }
   __device__ __forceinline__ void mark(int i) {
-    if (threadIdx.x == 0) {
+    if ((threadIdx.x & 127) == 0) {
       const long long now = clock64();
       ph[i] += now - t;
       t = now;
     }
   }
   __device__ __forceinline__ void flush(unsigned long long* out) {
-    if (threadIdx.x == 0 && out)
+    if ((threadIdx.x & 127) == 0 && out)
       for (int i = 0; i < 9; ++i) atomicAdd(out + i, ph[i]);
   }
-  __device__ __forceinline__ void step() { ph[8] += threadIdx.x == 0; }
+  __device__ __forceinline__ void step() { ph[8] += (threadIdx.x & 127) == 0; }
 #else
   __device__ __forceinline__ void step() {}
   __device__ __forceinline__ void start() {}
@@ -270,7 +312,14 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
   const int s0 = (r0 - C::W - base) % C::RING;
   constexpr int TAPS_IN = C::KC + 2 * C::W;
   constexpr int ELEMS = ModNext<C>::ELEMS;
-  constexpr int STRIDE = TAPS_IN / ELEMS > 0 ? TAPS_IN / ELEMS : 1;
+  static_assert(ELEMS % 4 == 0, "modulation batches of 4");
+  constexpr int NBATCH = ELEMS / 4;
+  constexpr int STRIDE = TAPS_IN / NBATCH > 0 ? TAPS_IN / NBATCH : 1;
+  // one batch of 4 modulation elements of the next step per STRIDE taps
+  auto batch = [&](int m) {
+    if (m % STRIDE == 0 && m / STRIDE < NBATCH)
+      ModNext<C>::template elements<4>(4 * (m / STRIDE), next.stage, next.M, next.n);
+  };
   auto ring = [&](int m) {
     int s = s0 + m;
     s = s >= C::RING ? s - C::RING : s;
@@ -281,15 +330,14 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
 #pragma unroll
     for (int m = 0; m <= 2 * C::W; ++m) {
       sum = add2(sum, ring(m));
-      if (m % STRIDE == 0 && m / STRIDE < ELEMS) next.element(m / STRIDE);
+      batch(m);
     }
     acc[0] = sum;
 #pragma unroll
     for (int i = 1; i < C::KC; ++i) {
       sum = sub2(add2(sum, ring(i + 2 * C::W)), ring(i - 1));
       acc[i] = sum;
-      const int m = i + 2 * C::W;
-      if (m % STRIDE == 0 && m / STRIDE < ELEMS) next.element(m / STRIDE);
+      batch(i + 2 * C::W);
     }
   } else {
 #pragma unroll
@@ -305,12 +353,12 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
           acc[i] = fma2(pk(tv, tv), v, acc[i]);
         }
       }
-      // one slice of the next step's modulation per STRIDE taps
-      if (m % STRIDE == 0 && m / STRIDE < ELEMS) next.element(m / STRIDE);
+      batch(m);
     }
   }
 #pragma unroll
-  for (int k = TAPS_IN / STRIDE + (TAPS_IN % STRIDE ? 1 : 0); k < ELEMS; ++k) next.element(k);
+  for (int b = TAPS_IN / STRIDE + (TAPS_IN % STRIDE ? 1 : 0); b < NBATCH; ++b)
+    ModNext<C>::template elements<4>(4 * b, next.stage, next.M, next.n);
   clk.mark(5);
   // (q, p) = c (Gc, Fc) + s (Gs, Fs)   [bilateral.hpp:138-144, real form]:
   // this lane's half of every row, then swap halves with the partner lane
