@@ -182,6 +182,13 @@ class Reference:
         L.ref_local_dynamic_range.argtypes = [_D, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.ref_error_bound.restype = ctypes.c_double
         L.ref_error_bound.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double]
+        L.ref_decode_pgm.argtypes = [ctypes.c_char_p, ctypes.c_size_t, _D, ctypes.c_size_t, _I, _I]
+        L.ref_cli_run.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_double, ctypes.c_double,
+                                  ctypes.c_double, ctypes.c_int, ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
+                                  ctypes.c_char_p, ctypes.c_int, ctypes.c_char_p, ctypes.c_size_t,
+                                  ctypes.c_char_p, ctypes.c_size_t]
+        L.ref_encode_pgm.restype = ctypes.c_long
+        L.ref_encode_pgm.argtypes = [_D, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_size_t]
         self.L = L
 
     def last_error(self):
@@ -249,3 +256,31 @@ class Reference:
 
     def error_bound(self, T, eps, w0):
         return self.L.ref_error_bound(T, eps, w0)
+
+    def decode_pgm(self, data: bytes):
+        """pgm.hpp decode_pgm -> ("ok", array HxW) or ("error", message)"""
+        cap = 1 << 22
+        v = np.zeros(cap)
+        w, h = ctypes.c_int(), ctypes.c_int()
+        if self.L.ref_decode_pgm(data, len(data), _dp(v), cap, ctypes.byref(w), ctypes.byref(h)):
+            return "error", self.last_error()
+        return "ok", v[: w.value * h.value].reshape(h.value, w.value).copy()
+
+    def encode_pgm(self, img) -> bytes:
+        a = _f64(img)
+        h, w = a.shape
+        buf = ctypes.create_string_buffer(w * h + 64)
+        n = self.L.ref_encode_pgm(_dp(a), w, h, buf, len(buf))
+        if n < 0:
+            raise ValueError(self.last_error())
+        return buf.raw[:n]
+
+    def cli_run(self, input_path, output_path="", sigma_s=1.0, sigma_r=30.0, epsilon=1e-3, family=0, table="",
+                spatial=0, compare_exact=False, report="", bench=False):
+        """cli.hpp run() -> (rc, stdout text, stderr text)"""
+        out = ctypes.create_string_buffer(1 << 16)
+        err = ctypes.create_string_buffer(1 << 12)
+        enc = lambda v: v.encode() if v else None  # noqa: E731
+        rc = self.L.ref_cli_run(enc(input_path), enc(output_path), sigma_s, sigma_r, epsilon, family, enc(table),
+                                spatial, int(compare_exact), enc(report), int(bench), out, len(out), err, len(err))
+        return rc, out.value.decode(), err.value.decode()

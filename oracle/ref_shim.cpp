@@ -15,6 +15,7 @@
 // they are reached).
 #include <algorithm>
 #include <cstring>
+#include <sstream>
 #include <exception>
 #include <numbers>
 #include <string>
@@ -23,8 +24,10 @@
 
 #include "fourierbf/analysis.hpp"
 #include "fourierbf/bilateral.hpp"
+#include "fourierbf/cli.hpp"
 #include "fourierbf/kernel_approx.hpp"
 #include "fourierbf/kernels.hpp"
+#include "fourierbf/pgm.hpp"
 #include "fourierbf/spatial.hpp"
 
 namespace fb = fourierbf;
@@ -233,6 +236,64 @@ double ref_error_bound(int T, double eps, double w0) {
         g_err = e.what();
         return -1.0;
     }
+}
+
+// pgm.hpp decode_pgm: 0 and the raster (up to cap values), or -1 with the
+// reference's message in ref_last_error()
+int ref_decode_pgm(const char* bytes, size_t len, double* values, size_t cap, int* w, int* h) {
+    try {
+        const fb::Image img = fb::decode_pgm(std::string_view(bytes, len));
+        *w = img.width;
+        *h = img.height;
+        std::memcpy(values, img.values.data(), sizeof(double) * std::min(cap, img.values.size()));
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// pgm.hpp encode_pgm: byte count (bytes copied up to cap), or -1
+long ref_encode_pgm(const double* values, int w, int h, char* out, size_t cap) {
+    try {
+        fb::Image img(w, h);
+        std::memcpy(img.values.data(), values, sizeof(double) * static_cast<size_t>(w) * h);
+        const std::string bytes = fb::encode_pgm(img);
+        std::memcpy(out, bytes.data(), std::min(cap, bytes.size()));
+        return static_cast<long>(bytes.size());
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// cli.hpp run(): the reference command-line driver on files (family 0 gaussian,
+// 1 exponential, 2 tabulated:<table>; spatial 0 gaussian, 1 box).  Returns
+// run()'s code; its stdout / stderr text is copied into out / err (cap bytes).
+int ref_cli_run(const char* input, const char* output, double sigma_s, double sigma_r, double epsilon,
+                int family, const char* table, int spatial, int compare_exact, const char* report, int bench,
+                char* out, size_t out_cap, char* err, size_t err_cap) {
+    fb::CliOptions opt;
+    opt.input_path = input ? input : "";
+    opt.output_path = output ? output : "";
+    opt.sigma_s = sigma_s;
+    opt.sigma_r = sigma_r;
+    opt.epsilon = epsilon;
+    opt.kernel_family = family == 2 ? fb::RangeFamily::tabulated
+                        : family == 1 ? fb::RangeFamily::exponential : fb::RangeFamily::gaussian;
+    opt.tabulated_path = table ? table : "";
+    opt.spatial_kind = spatial == 1 ? fb::SpatialKind::box : fb::SpatialKind::gaussian;
+    opt.compare_exact = compare_exact != 0;
+    opt.report_path = report ? report : "";
+    opt.bench = bench != 0;
+    std::ostringstream o, e;
+    const int rc = fb::run(opt, o, e);
+    const std::string so = o.str(), se = e.str();
+    std::memset(out, 0, out_cap);
+    std::memset(err, 0, err_cap);
+    std::memcpy(out, so.data(), std::min(out_cap - 1, so.size()));
+    std::memcpy(err, se.data(), std::min(err_cap - 1, se.size()));
+    return rc;
 }
 
 }  // extern "C"

@@ -314,7 +314,7 @@ int check_filter(const fbf_filter* f) {
   if (f->radius < 1 || f->radius > kMaxW)
     return fail(FBF_EUNSUPPORTED, "bilateral_fast: spatial radius outside [1, 64]");
   if (f->N < 0 || f->N > kMaxN)
-    return fail(FBF_EUNSUPPORTED, "bilateral_fast: harmonic count outside [0, 127]");
+    return fail(FBF_EUNSUPPORTED, "bilateral_fast: harmonic count outside [0, 65535]");
   if (f->check_epsilon && !(f->max_pointwise_error < f->w0))
     return fail(FBF_EINVAL,
                 "bilateral_fast: kernel approximation error must stay below the center "
@@ -369,7 +369,8 @@ void fill_taps(Taps& k, const fbf_filter* f) {
 void fill_harmonics(Harmonics& h, const fbf_filter* f) {
   std::memset(&h, 0, sizeof(h));
   h.N = f->N;
-  for (int n = 0; n <= f->N; ++n) h.d[n] = static_cast<float>(f->d[n]);
+  h.d_base = 0;
+  for (int n = 0; n <= f->N && n < kMaxD; ++n) h.d[n] = static_cast<float>(f->d[n]);
   h.turns_per_unit = f->omega / (2.0 * M_PI);
   h.shift = 128.0f;
   h.q_floor = static_cast<float>((f->w0 - f->max_pointwise_error) / 2.0);
@@ -507,6 +508,30 @@ struct Prepared {
   Layout L;
 };
 
+// Fused launches over harmonics [n_lo, n_hi): one launch when the range fits
+// the kMaxD coefficients of a parameter block (the common case, N < 256),
+// otherwise consecutive launches of kMaxD harmonics that keep accumulating
+// into the (Q, P) planes, the last one dividing unless `partial`.  Returns
+// the number of (Q, P) group planes left for finish_groups (1: none needed).
+int launch_fused_range(const FusedArgs& base, const fbf_filter* f, int n_lo, int n_hi, int groups, bool partial,
+                       cudaStream_t st, cudaError_t* err) {
+  FusedArgs A = base;
+  const bool one = n_hi - n_lo <= kMaxD;
+  A.groups = one ? std::max(1, std::min(groups, n_hi - n_lo)) : 1;
+  for (int c0 = n_lo; c0 < n_hi; c0 += kMaxD) {
+    const int c1 = std::min(n_hi, c0 + kMaxD);
+    A.n_lo = c0;
+    A.n_hi = c1;
+    A.h.d_base = c0;
+    for (int n = c0; n < c1; ++n) A.h.d[n - c0] = static_cast<float>(f->d[n]);
+    A.accumulate = c0 > n_lo;
+    A.partial = partial || A.groups > 1 || c1 < n_hi;
+    *err = launch_fused(A, st, nullptr);
+    if (*err != cudaSuccess) return 0;
+  }
+  return A.groups;
+}
+
 int prepare_common(const fbf_geometry* gp, const fbf_filter* f, void* workspace,
                    size_t workspace_bytes, int variant, Prepared& P) {
   int rc = check_geometry(gp);
@@ -573,17 +598,15 @@ int fbf_filter_prepared_device(const fbf_geometry* gp, const fbf_filter* f, floa
     A.pq = P.pq;
     A.bad = d_bad;
     A.seg_max = 1 << 30;
-    A.n_lo = 0;
-    A.n_hi = P.H.N + 1;
-    A.groups = std::min(harmonic_groups(gp, f->radius), P.H.N + 1);
-    A.partial = A.groups > 1;
-    FBF_CUDA(launch_fused(A, st, nullptr));
-    if (A.groups > 1) {
+    cudaError_t e = cudaSuccess;
+    const int groups = launch_fused_range(A, f, 0, P.H.N + 1, harmonic_groups(gp, f->radius), false, st, &e);
+    FBF_CUDA(e);
+    if (groups > 1) {
       const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
       const long long plane = static_cast<long long>(P.G.batch) * P.G.out_rows * cols;
       const long long out_px = static_cast<long long>(P.G.batch) * P.G.out_rows * P.G.width;
-      finish_groups<<<grid_for(out_px, 256), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), A.groups,
-                                                          A.n_hi - A.n_lo, plane, cols, P.G, P.H.shift,
+      finish_groups<<<grid_for(out_px, 256), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), groups,
+                                                          P.H.N + 1, plane, cols, P.G, P.H.shift,
                                                           P.H.q_floor, d_bad, dst, nullptr);
       FBF_CUDA(cudaGetLastError());
     }
@@ -602,7 +625,8 @@ int fbf_filter_prepared_device(const fbf_geometry* gp, const fbf_filter* f, floa
     naive_modulate<<<grid_for(src_px, 256), 256, 0, st>>>(P.uf, M, src_px, static_cast<uint32_t>(n));
     naive_rows<<<grid_for(src_px, 256), 256, 0, st>>>(M, T, NA);
     naive_cols<<<grid_for(out_px, 256), 256, 0, st>>>(T, C, NA);
-    naive_demod<<<grid_for(out_px, 256), 256, 0, st>>>(M, C, reinterpret_cast<p2*>(P.pq), P.Gd, P.H.d[n], n == 0);
+    naive_demod<<<grid_for(out_px, 256), 256, 0, st>>>(M, C, reinterpret_cast<p2*>(P.pq), P.Gd,
+                                                       static_cast<float>(f->d[n]), n == 0);
   }
   finish_kernel<<<grid_for(out_px, 256), 256, 0, st>>>(reinterpret_cast<p2*>(P.pq), dst, P.G, P.H.shift, P.H.q_floor, d_bad);
   FBF_CUDA(cudaGetLastError());
@@ -635,14 +659,12 @@ int fbf_partial_sums_device(const fbf_geometry* gp, const fbf_filter* f, int n_l
     A.uf = P.uf;
     A.pq = P.pq;
     A.seg_max = 1 << 30;
-    A.n_lo = n_lo;
-    A.n_hi = n_hi;
-    A.groups = std::min(harmonic_groups(gp, f->radius), n_hi - n_lo);
-    A.partial = 1;
-    FBF_CUDA(launch_fused(A, st, nullptr));
+    cudaError_t e = cudaSuccess;
+    const int groups = launch_fused_range(A, f, n_lo, n_hi, harmonic_groups(gp, f->radius), true, st, &e);
+    FBF_CUDA(e);
     const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
     const long long plane = static_cast<long long>(P.G.batch) * P.G.out_rows * cols;
-    finish_groups<<<grid_for(out_px, 256), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), A.groups,
+    finish_groups<<<grid_for(out_px, 256), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), groups,
                                                         n_hi - n_lo, plane, cols, P.G, 0.f, 0.f, nullptr,
                                                         nullptr, reinterpret_cast<p2*>(pq_out));
     FBF_CUDA(cudaGetLastError());
@@ -659,8 +681,8 @@ int fbf_partial_sums_device(const fbf_geometry* gp, const fbf_filter* f, int n_l
     naive_modulate<<<grid_for(src_px, 256), 256, 0, st>>>(P.uf, M, src_px, static_cast<uint32_t>(n));
     naive_rows<<<grid_for(src_px, 256), 256, 0, st>>>(M, T, NA);
     naive_cols<<<grid_for(out_px, 256), 256, 0, st>>>(T, Cc, NA);
-    naive_demod<<<grid_for(out_px, 256), 256, 0, st>>>(M, Cc, reinterpret_cast<p2*>(pq_out), P.Gd, P.H.d[n],
-                                                       n == n_lo);
+    naive_demod<<<grid_for(out_px, 256), 256, 0, st>>>(M, Cc, reinterpret_cast<p2*>(pq_out), P.Gd,
+                                                       static_cast<float>(f->d[n]), n == n_lo);
   }
   FBF_CUDA(cudaGetLastError());
   return FBF_OK;
@@ -683,8 +705,11 @@ int fbf_finish_device(const fbf_geometry* gp, const fbf_filter* f, const float* 
 
 int fbf_launches_per_call(const fbf_geometry* g, const fbf_filter* f, int variant) {
   if (!f || !g) return 0;
-  if (variant == FBF_VARIANT_FUSED && fused_supported(f->radius, f->kind == FBF_SPATIAL_BOX))
+  if (variant == FBF_VARIANT_FUSED && fused_supported(f->radius, f->kind == FBF_SPATIAL_BOX)) {
+    const int chunks = (f->N + kMaxD) / kMaxD;  // fused launches of <= kMaxD harmonics
+    if (chunks > 1) return 1 + chunks;
     return std::min(harmonic_groups(g, f->radius), f->N + 1) > 1 ? 3 : 2;  // prep, fused (, group sum)
+  }
   return 1 + 4 * (f->N + 1) + 1;
 }
 

@@ -1,0 +1,215 @@
+// fbf_cli.cpp -- the PGM codec and the command-line driver of the drop-in
+// C++ API (include/fourierbf/pgm.hpp, cli.hpp; reference:
+// proj/include/fourierbf/pgm.hpp:62-133, cli.hpp:24-142).  The filtering
+// itself is the B200 pipeline behind filter() / bilateral_fast() /
+// bilateral_exact() (fbf_host.cpp -> C-ABI -> CUDA); nothing here computes
+// pixels.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <fstream>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+
+#include "fourierbf/analysis.hpp"
+#include "fourierbf/bilateral.hpp"
+#include "fourierbf/cli.hpp"
+#include "fourierbf/kernel_approx.hpp"
+#include "fourierbf/pgm.hpp"
+
+namespace fourierbf {
+
+namespace {
+
+// ------------------------------------------------------------------ PGM
+
+[[noreturn]] void parse_error(std::size_t at, const std::string& what) {
+    throw std::runtime_error("pgm parse error at byte " + std::to_string(at) + ": " + what);
+}
+
+bool is_pgm_space(char c) {
+    return c == ' ' || c == '\t' || c == '\n' || c == '\r' || c == '\v' || c == '\f';
+}
+
+// Header / ASCII-raster tokenizer: whitespace and '#'-to-end-of-line comments
+// separate unsigned decimal fields.
+class Scanner {
+public:
+    explicit Scanner(std::string_view s, std::size_t at) : s_(s), at_(at) {}
+    std::size_t at() const { return at_; }
+    bool done() const { return at_ >= s_.size(); }
+    char cur() const { return s_[at_]; }
+    void advance() { ++at_; }
+
+    long field(const char* name) {
+        for (;;) {  // skip separators
+            if (done()) parse_error(at_, std::string("missing ") + name);
+            if (cur() == '#') {
+                while (!done() && cur() != '\n') ++at_;
+            } else if (is_pgm_space(cur())) {
+                ++at_;
+            } else {
+                break;
+            }
+        }
+        if (cur() < '0' || cur() > '9') parse_error(at_, std::string("expected digit for ") + name);
+        long v = 0;
+        while (!done() && cur() >= '0' && cur() <= '9') {
+            v = 10 * v + (cur() - '0');
+            if (v > 1000000000L) parse_error(at_, std::string(name) + " out of range");
+            ++at_;
+        }
+        return v;
+    }
+
+private:
+    std::string_view s_;
+    std::size_t at_;
+};
+
+// ------------------------------------------------------------------ CLI
+
+RangeKernel range_for(const CliOptions& opt, double sigma_r) {
+    switch (opt.kernel_family) {
+        case RangeFamily::gaussian: return RangeKernel::gaussian(sigma_r);
+        case RangeFamily::exponential: return RangeKernel::exponential(sigma_r);
+        case RangeFamily::tabulated: return RangeKernel::tabulated_from_file(opt.tabulated_path);
+    }
+    throw std::logic_error("unknown range kernel family");
+}
+
+SpatialKernel spatial_for(const CliOptions& opt, double sigma_s) {
+    if (!(sigma_s > 0.0)) throw std::invalid_argument("--sigma-s must be positive");
+    return opt.spatial_kind == SpatialKind::box ? make_spatial_box(static_cast<int>(std::ceil(sigma_s)))
+                                                : make_spatial_gaussian(sigma_s);
+}
+
+// cli.hpp:72-100: the two sweeps of the paper's timing tables, one fast-filter
+// call each (T from the image, progressive fit at --epsilon), CSV rows
+// "param,value,millis".  The timed call is bilateral_fast on the GPU with host
+// buffers in and out (what a caller of the C++ API pays).
+void bench_sweeps(const CliOptions& opt, const Image& image, std::ostream& out) {
+    if (opt.kernel_family == RangeFamily::tabulated)
+        throw std::invalid_argument("--bench needs a parametric kernel family to sweep sigma_r");
+    out << "param,value,millis\n";
+    auto timed = [&](const char* param, double value, double sigma_s, double sigma_r) {
+        const SpatialKernel spatial = spatial_for(opt, sigma_s);
+        const RangeKernel range = range_for(opt, sigma_r);
+        const int T = std::max(local_dynamic_range(image, spatial.radius), 1);
+        const FourierKernelApprox approx = progressive_fit(range, T, opt.epsilon);
+        const auto t0 = std::chrono::steady_clock::now();
+        const Image filtered = bilateral_fast(image, spatial, approx, opt.backend);
+        const auto t1 = std::chrono::steady_clock::now();
+        (void)filtered;
+        char line[96];
+        std::snprintf(line, sizeof line, "%s,%g,%.3f\n", param, value,
+                      std::chrono::duration<double, std::milli>(t1 - t0).count());
+        out << line;
+    };
+    for (const double s : {1.0, 2.0, 5.0, 8.0, 10.0, 12.0}) timed("sigma_s", s, s, opt.sigma_r);
+    for (const double r : {10.0, 15.0, 20.0, 30.0, 50.0, 100.0}) timed("sigma_r", r, opt.sigma_s, r);
+}
+
+}  // namespace
+
+Image decode_pgm(std::string_view bytes) {
+    if (bytes.size() < 2 || bytes[0] != 'P' || (bytes[1] != '5' && bytes[1] != '2'))
+        parse_error(0, "not a P5 or P2 graymap");
+    const bool raw = bytes[1] == '5';
+    Scanner sc(bytes, 2);
+    const long w = sc.field("width");
+    const long h = sc.field("height");
+    const long maxval = sc.field("maxval");
+    if (w < 1 || h < 1) parse_error(sc.at(), "non-positive dimensions");
+    if (w > (1L << 20) || h > (1L << 20)) parse_error(sc.at(), "dimensions out of range");
+    if (maxval < 1 || maxval > 255) parse_error(sc.at(), "maxval must be in [1, 255]");
+    Image img(static_cast<int>(w), static_cast<int>(h));
+    const std::size_t n = img.values.size();
+    if (raw) {
+        // exactly one whitespace byte separates the header from the raster
+        if (sc.done()) parse_error(sc.at(), "missing raster");
+        if (!(sc.cur() == ' ' || sc.cur() == '\t' || sc.cur() == '\n' || sc.cur() == '\r'))
+            parse_error(sc.at(), "expected whitespace before raster");
+        const std::size_t start = sc.at() + 1;
+        if (bytes.size() - start < n)
+            parse_error(bytes.size(), "truncated raster, expected " + std::to_string(n) + " bytes after header");
+        for (std::size_t i = 0; i < n; ++i) {
+            const unsigned v = static_cast<unsigned char>(bytes[start + i]);
+            if (v > static_cast<unsigned long>(maxval)) parse_error(start + i, "sample exceeds maxval");
+            img.values[i] = static_cast<double>(v);
+        }
+    } else {
+        for (std::size_t i = 0; i < n; ++i) {
+            const long v = sc.field("sample");
+            if (v > maxval) parse_error(sc.at(), "sample exceeds maxval");
+            img.values[i] = static_cast<double>(v);
+        }
+    }
+    return img;
+}
+
+std::string encode_pgm(const Image& img) {
+    if (img.width <= 0 || img.height <= 0) throw std::invalid_argument("encode_pgm: empty image");
+    std::string bytes = "P5\n" + std::to_string(img.width) + " " + std::to_string(img.height) + "\n255\n";
+    const std::size_t header = bytes.size();
+    bytes.resize(header + img.values.size());
+    for (std::size_t i = 0; i < img.values.size(); ++i) {
+        const double q = std::clamp(std::floor(img.values[i] + 0.5), 0.0, 255.0);
+        bytes[header + i] = static_cast<char>(static_cast<unsigned char>(q));
+    }
+    return bytes;
+}
+
+Image read_pgm(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw std::runtime_error("cannot open " + path + " for reading");
+    std::ostringstream all;
+    all << f.rdbuf();
+    if (!f.good() && !f.eof()) throw std::runtime_error("read failure on " + path);
+    return decode_pgm(all.str());
+}
+
+void write_pgm(const Image& img, const std::string& path) {
+    const std::string bytes = encode_pgm(img);
+    std::ofstream f(path, std::ios::binary | std::ios::trunc);
+    if (!f) throw std::runtime_error("cannot open " + path + " for writing");
+    f.write(bytes.data(), static_cast<std::streamsize>(bytes.size()));
+    if (!f) throw std::runtime_error("write failure on " + path);
+}
+
+// cli.hpp:106-140
+int run(const CliOptions& opt, std::ostream& out, std::ostream& err) {
+    try {
+        if (opt.input_path.empty()) throw std::invalid_argument("--input is required");
+        if (opt.output_path.empty() && !opt.bench)
+            throw std::invalid_argument("--output is required unless --bench is set");
+        if (opt.kernel_family != RangeFamily::tabulated && !(opt.sigma_r > 0.0))
+            throw std::invalid_argument("--sigma-r must be positive");
+        if (!(opt.epsilon > 0.0)) throw std::invalid_argument("--epsilon must be positive");
+
+        const Image image = read_pgm(opt.input_path);
+        if (opt.bench) bench_sweeps(opt, image, out);
+        if (opt.output_path.empty()) return 0;
+
+        const FilterConfig config{spatial_for(opt, opt.sigma_s), range_for(opt, opt.sigma_r), opt.epsilon, true,
+                                  opt.backend};
+        auto [filtered, report] = filter(image, config);
+        if (opt.compare_exact)
+            report.measured_linf = linf_error(bilateral_exact(image, config.spatial, config.range), filtered);
+        write_pgm(filtered, opt.output_path);
+        if (!opt.report_path.empty()) {
+            std::ofstream rep(opt.report_path, std::ios::trunc);
+            if (!rep) throw std::runtime_error("cannot open " + opt.report_path + " for writing");
+            report.write_key_values(rep);
+            if (!rep.good()) throw std::runtime_error("write failure on " + opt.report_path);
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        err << "error: " << e.what() << '\n';
+        return 1;
+    }
+}
+
+}  // namespace fourierbf

@@ -298,7 +298,7 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restric
 template <class C>
 __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restrict__ R,
                                          const float* __restrict__ CS, const p2* __restrict__ pqs,
-                                         const Unit& u, int o, int base, int n, bool first, bool divide,
+                                         const Unit& u, int o, int base, int dn_idx, bool first, bool divide,
                                          const ModNext<C>& next, PhaseClock& clk) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int h = lane >> 4;
@@ -384,7 +384,8 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
   const int nh = nr - h * KH;  // rows of this lane (may be <= 0)
   if (nh <= 0) return;
   // box: both passes summed unweighted; the weight (1/(2W+1))^2 = w0 joins d_n here
-  const float dn = C::BOX ? A.h.d[n] * (A.k.box_tap * A.k.box_tap) : A.h.d[n];
+  // d_n (dn_idx = n - d_base: the launch's coefficient block)
+  const float dn = C::BOX ? A.h.d[dn_idx] * (A.k.box_tap * A.k.box_tap) : A.h.d[dn_idx];
   const p2 dd = pk(dn, dn);
   const p2* __restrict__ pqin = pqs + (gi + h * KH) * C::TW + x;
   if (!divide) {
@@ -449,6 +450,9 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
   const int nb = A.n_lo + span * static_cast<int>(blockIdx.y) / A.groups;
   const int ne = A.n_lo + span * static_cast<int>(blockIdx.y + 1) / A.groups;
   if (nb >= ne) return;
+  // the harmonic whose (Q, P) initialises the planes (none for a chained launch
+  // that accumulates onto an earlier one)
+  const int n_first = A.accumulate ? -1 : nb;
 
   const long long total = A.total;
   // CTA ranges in (strip, row) space, with the row rounded down to a multiple
@@ -488,7 +492,7 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
       modulate_rows<C>(stage, M, rows, static_cast<uint32_t>(nb));
     }
     for (int n = nb; n < ne; ++n) {
-      const bool first = n == nb;
+      const bool first = n == n_first;
       const bool divide = n + 1 == ne && !A.partial;
       for (int s = 0; s < nsteps; ++s) {
         int a, rows, o, a2, rows2, o2;
@@ -522,7 +526,7 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
         // (its ALU work issues in the FFMA2 shadow); prologue steps run it alone
         const ModNext<C> next{stage, M, static_cast<uint32_t>(wrap ? n + 1 : n)};
         if (o >= 0) {
-          col_pass<C>(A, R, CS, pqs, u, o, base, n, first, divide, next, clk);
+          col_pass<C>(A, R, CS, pqs, u, o, base, n - A.h.d_base, first, divide, next, clk);
           clk.mark(7);
         } else {
           modulate_rows<C>(stage, M, rows2, next.n);

@@ -7,7 +7,8 @@
 
 namespace fbf {
 
-constexpr int kMaxN = 127;  // highest harmonic supported by one launch
+constexpr int kMaxD = 256;     // harmonic coefficients carried by one fused launch
+constexpr int kMaxN = 65535;   // highest harmonic accepted (larger N: several fused launches)
 constexpr int kFusedTW = 64;  // column-strip width of the fused kernel (workspace layout)
 constexpr int kMaxW = 64;   // largest spatial radius supported by the fused/naive paths
 
@@ -33,7 +34,8 @@ struct Geometry {
 
 struct Harmonics {
   int N;
-  float d[kMaxN + 1];  // cosine coefficients d_0..d_N (fp32)
+  int d_base;          // d[i] is the coefficient of harmonic d_base + i
+  float d[kMaxD];      // cosine coefficients d_base .. d_base + kMaxD - 1 (fp32)
   double turns_per_unit;  // omega / (2 pi): phase in turns per intensity unit
   float shift;            // intensity shift applied before modulation (128)
   float q_floor;          // (w0 - eps) / 2 : denominator collapse threshold
@@ -63,7 +65,6 @@ struct FusedArgs {
   int groups;
   int partial;
   Geometry g;
-  Harmonics h;
   Taps k;
   const int2* uf;          // prep output: (u = phase increment, f' bits)
   float* dst;
@@ -73,6 +74,8 @@ struct FusedArgs {
   long long total;         // batch * strips * out_rows
   int seg_max;             // longest row run one CTA filters in one pass over n
   unsigned long long* prof;  // phase cycle counters (FBF_PHASE_PROF builds only), else null
+  int accumulate;  // 1: the launch's first harmonic adds to the (Q, P) planes instead of initialising them
+  Harmonics h;     // last: the coefficient block is the large member
 };
 
 }  // namespace fbf

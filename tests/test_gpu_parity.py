@@ -201,3 +201,34 @@ def test_convolve_matches_oracle(oracle):
                       ((9, 1), fb.make_spatial_box(4)), ((300, 257), fb.make_spatial_gaussian(8.0))):
         img = rng.random(shape) * 255
         assert maxabs(fb.convolve(img, sk), oracle.convolve(img, sk.profile, sk.radius)) <= 1e-3
+
+
+@pytest.mark.parametrize("variant", ["fused", "naive"])
+def test_harmonic_count_beyond_one_launch(oracle, variant):
+    """N up to T (progressive_fit's limit, kernel_approx.hpp:189-203): a dynamic
+    range of 600 and N = 300 -> the fused path runs two chained launches of
+    <= 256 harmonics (the second accumulating onto the first's (Q, P))."""
+    rng = np.random.default_rng(600)
+    img = np.clip(rng.normal(300, 120, (40, 72)), 0, 600)
+    img[8:30, 20:50] += 150
+    img = np.minimum(img, 600.0)
+    s = fb.make_spatial_gaussian(1.5)
+    a = fb.fit_fixed(fb.RANGE_GAUSSIAN, 40.0, 600, 300)
+    assert a.N == 300
+    gpu = fb.bilateral_fast(img, s, a, variant=variant)
+    # fp32 over a range 600/255 times wider than 8-bit images
+    assert maxabs(gpu, oracle_rows(oracle, img, s, a)) <= TOL * 600 / 255
+
+
+def test_exponential_kernel_high_order(oracle):
+    """the CLI's box / exponential case: progressive_fit picks N > 127"""
+    rng = np.random.default_rng(25)
+    img = np.floor(np.clip(rng.normal(120, 50, (40, 48)), 0, 255) + 0.5)
+    s = fb.make_spatial_box(2)
+    T = oracle.local_dynamic_range(img, s.radius)
+    d, N, _, mx = oracle.progressive_fit(1, 25.0, T, 1e-3)
+    assert N > 127
+    a = fb.progressive_fit(fb.RANGE_EXPONENTIAL, 25.0, T, 1e-3)
+    assert a.N == N
+    gpu = fb.bilateral_fast(img, s, a)
+    assert maxabs(gpu, oracle_rows(oracle, img, s, a)) <= TOL
