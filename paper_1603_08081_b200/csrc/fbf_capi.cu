@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "fbf_device.cuh"
 #include "fbf_params.h"
@@ -47,7 +48,9 @@ size_t align256(size_t n) { return (n + 255) & ~size_t(255); }
 // pool trimming inside repeated calls.  fbf_release_host_buffers() frees them.
 struct HostCtx {
   int dev = -1;
-  cudaStream_t st = nullptr;
+  cudaStream_t st = nullptr;   // chunk stream 0
+  cudaStream_t st2 = nullptr;  // chunk stream 1 (copies of one chunk overlap the kernels of the other)
+  cudaEvent_t ev[2] = {nullptr, nullptr};
   char* buf = nullptr;
   size_t cap = 0;
 };
@@ -74,10 +77,13 @@ int host_ctx(size_t bytes, HostCtx*& out) {
     g_host = HostCtx{};
     g_host.dev = dev;
     FBF_CUDA(cudaStreamCreateWithFlags(&g_host.st, cudaStreamNonBlocking));
+    FBF_CUDA(cudaStreamCreateWithFlags(&g_host.st2, cudaStreamNonBlocking));
+    for (auto& e : g_host.ev) FBF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   if (g_host.cap < bytes) {
     if (g_host.buf) {
       cudaStreamSynchronize(g_host.st);
+      cudaStreamSynchronize(g_host.st2);
       cudaFree(g_host.buf);
       g_host.buf = nullptr;
       g_host.cap = 0;
@@ -713,6 +719,59 @@ int fbf_launches_per_call(const fbf_geometry* g, const fbf_filter* f, int varian
   return 1 + 4 * (f->N + 1) + 1;
 }
 
+// Host-buffer entry point, pipelined: the work is cut into K chunks (whole
+// images of a batch, or row strips of one large image) issued alternately on
+// two streams, so chunk k's H2D / D2H copies overlap the kernels of its
+// neighbours.  Row strips carry their W halo rows (mirror only at the global
+// edges) and are cut on multiples of 16 rows: the fused kernel's results do
+// not depend on the cut (tests/test_gpu_device.py), so K only changes speed.
+// Batches: up to 8 image chunks.  One image: K strips from a measured cost
+// model (plan_chunks).
+namespace {
+
+struct Chunk {
+  int b0, nb;     // images [b0, b0 + nb)
+  int o0, o1;     // output rows (global) [o0, o1)
+  int s0, s1;     // source rows (global) [s0, s1) held on the device for this chunk
+};
+
+std::vector<Chunk> plan_chunks(const fbf_geometry* g, int W, int variant) {
+  std::vector<Chunk> c;
+  const double px = static_cast<double>(g->width) * g->out_rows * g->batch;
+  if (variant != FBF_VARIANT_FUSED || px < 2.0e6) {  // small: one launch
+    c.push_back({0, g->batch, g->out_row0, g->out_row0 + g->out_rows, g->src_row0, g->src_row0 + g->src_rows});
+    return c;
+  }
+  if (g->batch >= 2) {  // whole images per chunk
+    const int k = std::min(g->batch, 8);
+    for (int i = 0; i < k; ++i) {
+      const int b0 = g->batch * i / k, b1 = g->batch * (i + 1) / k;
+      if (b1 > b0)
+        c.push_back({b0, b1 - b0, g->out_row0, g->out_row0 + g->out_rows, g->src_row0, g->src_row0 + g->src_rows});
+    }
+    return c;
+  }
+  // one image: K strips cost ~ a + b/K + c*K (b: the copies a strip pipeline
+  // hides, c: per-strip prologue rows, launch and tail); fitted on c2 / c4
+  // (profiles/r01_notes.md): K ~ sqrt(b/c) ~ sqrt(pixels / 0.45 M), at most 6
+  int best = static_cast<int>(std::lround(std::sqrt(px / 0.45e6)));
+  best = std::max(1, std::min(best, 6));
+  if (const char* force = getenv("FBF_HOST_CHUNKS")) best = std::max(1, atoi(force));  // experiments
+  while (best > 1 && g->out_rows / best < 4 * W + 16) --best;
+  for (int i = 0; i < best; ++i) {
+    int o0 = g->out_row0 + (g->out_rows * i / best) / 16 * 16;
+    int o1 = i + 1 == best ? g->out_row0 + g->out_rows : g->out_row0 + (g->out_rows * (i + 1) / best) / 16 * 16;
+    if (i == 0) o0 = g->out_row0;
+    if (o1 <= o0) continue;
+    const int s0 = std::max(g->src_row0, std::max(0, o0 - W));
+    const int s1 = std::min(g->src_row0 + g->src_rows, std::min(g->height, o1 + W));
+    c.push_back({0, 1, o0, o1, s0, s1});
+  }
+  return c;
+}
+
+}  // namespace
+
 int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const float* src,
                             float* dst, int variant, long long* bad_index) {
   int rc = check_geometry(g);
@@ -721,67 +780,118 @@ int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const fl
   if ((rc = check_halo(g, f->radius))) return rc;
   int v = variant;
   if (v == FBF_VARIANT_FUSED && !fused_supported(f->radius, f->kind == FBF_SPATIAL_BOX)) v = FBF_VARIANT_NAIVE;
-  // device buffers: dense copies of the source rows and output rows
-  fbf_geometry gd = *g;
-  gd.src_pitch = g->width;
-  gd.dst_pitch = g->width;
-  gd.src_bstride = static_cast<long long>(g->src_rows) * g->width;
-  gd.dst_bstride = static_cast<long long>(g->out_rows) * g->width;
-  const size_t src_bytes = static_cast<size_t>(gd.src_bstride) * g->batch * sizeof(float);
-  const size_t dst_bytes = static_cast<size_t>(gd.dst_bstride) * g->batch * sizeof(float);
-  const size_t ws_bytes = layout_of(&gd, f->radius, v).total;
-  const size_t total = align256(src_bytes) + align256(dst_bytes) + ws_bytes + 256;
+  const std::vector<Chunk> chunks = plan_chunks(g, f->radius, v);
+  const int K = static_cast<int>(chunks.size());
+  // device buffers: dense copies of the source rows and output rows of the whole call
+  const long long sb = static_cast<long long>(g->src_rows) * g->width;  // per image
+  const long long db = static_cast<long long>(g->out_rows) * g->width;
+  const size_t src_bytes = static_cast<size_t>(sb) * g->batch * sizeof(float);
+  const size_t dst_bytes = static_cast<size_t>(db) * g->batch * sizeof(float);
+  auto chunk_geometry = [&](const Chunk& c) {
+    fbf_geometry gc = *g;
+    gc.batch = c.nb;
+    gc.src_row0 = c.s0;
+    gc.src_rows = c.s1 - c.s0;
+    gc.out_row0 = c.o0;
+    gc.out_rows = c.o1 - c.o0;
+    gc.src_pitch = g->width;
+    gc.dst_pitch = g->width;
+    gc.src_bstride = sb;
+    gc.dst_bstride = db;
+    return gc;
+  };
+  size_t ws_bytes = 0;
+  for (const Chunk& c : chunks) {
+    const fbf_geometry gc = chunk_geometry(c);
+    ws_bytes = std::max(ws_bytes, align256(layout_of(&gc, f->radius, v).total));
+  }
+  const int nws = K > 1 ? 2 : 1;
+  const size_t total = align256(src_bytes) + align256(dst_bytes) + nws * ws_bytes + align256(K * 8) + 256;
   HostCtx* ctx = nullptr;
   if ((rc = host_ctx(total, ctx))) return rc;
-  cudaStream_t st = ctx->st;
+  cudaStream_t sts[2] = {ctx->st, ctx->st2};
   char* buf = ctx->buf;
-  cudaError_t e = cudaSuccess;
   float* d_src = reinterpret_cast<float*>(buf);
   float* d_dst = reinterpret_cast<float*>(buf + align256(src_bytes));
-  void* ws = buf + align256(src_bytes) + align256(dst_bytes);
-  unsigned long long* d_bad =
-      reinterpret_cast<unsigned long long*>(buf + align256(src_bytes) + align256(dst_bytes) + ws_bytes);
+  char* ws0 = buf + align256(src_bytes) + align256(dst_bytes);
+  unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(ws0 + nws * ws_bytes);
+  std::vector<unsigned long long> bad(K, ~0ULL);
+  cudaError_t e = cudaSuccess;
   int out = FBF_OK;
+  int copied_hi = g->src_row0;  // row strips: source rows already on their way to the device
   do {
-    for (int b = 0; b < g->batch; ++b) {
-      e = cudaMemcpy2DAsync(d_src + b * gd.src_bstride, g->width * sizeof(float),
-                            src + b * g->src_bstride, g->src_pitch * sizeof(float),
-                            g->width * sizeof(float), g->src_rows, cudaMemcpyHostToDevice, st);
-      if (e != cudaSuccess) break;
-    }
-    if (e != cudaSuccess) { out = cuda_fail(e, "H2D"); break; }
-    e = cudaMemsetAsync(d_bad, 0xFF, sizeof(unsigned long long), st);
+    e = cudaMemsetAsync(d_bad, 0xFF, K * sizeof(unsigned long long), sts[0]);
+    if (e == cudaSuccess && K > 1) e = cudaEventRecord(ctx->ev[1], sts[0]);
+    if (e == cudaSuccess && K > 1) e = cudaStreamWaitEvent(sts[1], ctx->ev[1], 0);
     if (e != cudaSuccess) { out = cuda_fail(e, "memset"); break; }
-    out = fbf_bilateral_fast_device(&gd, f, d_src, d_dst, ws, ws_bytes, d_bad, v, st);
-    if (out != FBF_OK) break;
-    for (int b = 0; b < g->batch; ++b) {
-      e = cudaMemcpy2DAsync(dst + b * g->dst_bstride, g->dst_pitch * sizeof(float),
-                            d_dst + b * gd.dst_bstride, g->width * sizeof(float),
-                            g->width * sizeof(float), g->out_rows, cudaMemcpyDeviceToHost, st);
-      if (e != cudaSuccess) break;
+    for (int k = 0; k < K && out == FBF_OK; ++k) {
+      const Chunk& c = chunks[k];
+      cudaStream_t st = sts[k & 1];
+      // H2D: this chunk's images, or the source rows no earlier strip has copied
+      const int r0 = g->batch >= 2 || K == 1 ? c.s0 : std::max(c.s0, copied_hi);
+      for (int b = c.b0; b < c.b0 + c.nb && r0 < c.s1; ++b) {
+        e = cudaMemcpy2DAsync(d_src + b * sb + static_cast<long long>(r0 - g->src_row0) * g->width,
+                              g->width * sizeof(float),
+                              src + b * g->src_bstride + static_cast<long long>(r0 - g->src_row0) * g->src_pitch,
+                              g->src_pitch * sizeof(float), g->width * sizeof(float), c.s1 - r0,
+                              cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) break;
+      }
+      if (e != cudaSuccess) { out = cuda_fail(e, "H2D"); break; }
+      if (g->batch < 2 && K > 1) {
+        // the strip's upper halo rows came with the previous strip, on the other stream
+        if (k > 0 && c.s0 < copied_hi) e = cudaStreamWaitEvent(st, ctx->ev[(k - 1) & 1], 0);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->ev[k & 1], st);
+        if (e != cudaSuccess) { out = cuda_fail(e, "event"); break; }
+        copied_hi = std::max(copied_hi, c.s1);
+      }
+      const fbf_geometry gc = chunk_geometry(c);
+      out = fbf_bilateral_fast_device(&gc, f, d_src + c.b0 * sb + static_cast<long long>(c.s0 - g->src_row0) * g->width,
+                                      d_dst + c.b0 * db + static_cast<long long>(c.o0 - g->out_row0) * g->width,
+                                      ws0 + (k & 1) * (nws > 1 ? ws_bytes : 0), ws_bytes, d_bad + k, v, st);
+      if (out != FBF_OK) break;
+      for (int b = c.b0; b < c.b0 + c.nb; ++b) {
+        e = cudaMemcpy2DAsync(dst + b * g->dst_bstride + static_cast<long long>(c.o0 - g->out_row0) * g->dst_pitch,
+                              g->dst_pitch * sizeof(float),
+                              d_dst + b * db + static_cast<long long>(c.o0 - g->out_row0) * g->width,
+                              g->width * sizeof(float), g->width * sizeof(float), c.o1 - c.o0,
+                              cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) break;
+      }
+      if (e != cudaSuccess) { out = cuda_fail(e, "D2H"); break; }
     }
-    if (e != cudaSuccess) { out = cuda_fail(e, "D2H"); break; }
-    unsigned long long bad = ~0ULL;
-    e = cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (out != FBF_OK) break;
+    e = cudaStreamSynchronize(sts[1]);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(bad.data(), d_bad, K * sizeof(unsigned long long),
+                                              cudaMemcpyDeviceToHost, sts[0]);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(sts[0]);
     if (e != cudaSuccess) { out = cuda_fail(e, "sync"); break; }
-    if (bad != ~0ULL) {
-      if (bad_index) *bad_index = static_cast<long long>(bad);
+    // chunk-local image index -> the call's (the kernels number images from 0 per launch)
+    const unsigned long long per_img = static_cast<unsigned long long>(g->width) * g->height;
+    for (int k = 0; k < K; ++k)
+      if (bad[k] != ~0ULL) bad[k] += static_cast<unsigned long long>(chunks[k].b0) * per_img;
+    const unsigned long long first_bad = *std::min_element(bad.begin(), bad.end());
+    if (first_bad != ~0ULL) {
+      if (bad_index) *bad_index = static_cast<long long>(first_bad);
       const long long per = static_cast<long long>(g->width) * g->height;
-      const long long inimg = static_cast<long long>(bad) % per;
+      const long long inimg = static_cast<long long>(first_bad) % per;
       const long long x = inimg % g->width, y = inimg / g->width;
       out = fail(FBF_EANOMALY,
                  "bilateral_fast: numerical anomaly, denominator collapsed at pixel (" +
                      std::to_string(x) + ", " + std::to_string(y) + ")");
     }
   } while (false);
-  cudaStreamSynchronize(st);
+  cudaStreamSynchronize(sts[0]);
+  cudaStreamSynchronize(sts[1]);
   return out;
 }
 
 void fbf_release_host_buffers(void) {
   if (g_host.buf) cudaFree(g_host.buf);
   if (g_host.st) cudaStreamDestroy(g_host.st);
+  if (g_host.st2) cudaStreamDestroy(g_host.st2);
+  for (auto e : g_host.ev)
+    if (e) cudaEventDestroy(e);
   g_host = HostCtx{};
   if (g_pinned) cudaFreeHost(g_pinned);
   g_pinned = nullptr;

@@ -63,3 +63,26 @@ def test_device_path_matches_host_path():
     img, s, a = image_of(c), spatial_of(c), approx_of(c)
     dev = run_device(img, fb.whole_geometry(c.width, c.height), s, a)[0]
     assert np.array_equal(dev, fb.bilateral_fast(img, s, a))
+
+
+@pytest.mark.parametrize("shape", [(1536, 2048), (3, 1024, 1024), (4096, 1024)])
+def test_pipelined_host_path_is_bit_identical(shape):
+    """fbf_bilateral_fast_host cuts > 2 Mpx calls into row strips (one image) or
+    image chunks (batches) on two streams so the copies overlap the kernels;
+    the result must not depend on the cut."""
+    c = CONFIGS["c2"]
+    s, a = spatial_of(c), approx_of(c)
+    rng = np.random.default_rng(sum(shape))
+    img = np.clip(rng.normal(128, 60, shape), 0, 255).astype(np.float32)
+    batch = 1 if len(shape) == 2 else shape[0]
+    h, w = shape[-2], shape[-1]
+    dev = run_device(img.reshape(batch, h, w), fb.whole_geometry(w, h, batch), s, a).reshape(shape)
+    assert np.array_equal(dev, fb.bilateral_fast(img, s, a))
+
+
+def test_pipelined_host_path_reports_the_first_collapse():
+    rng = np.random.default_rng(9)
+    img = rng.integers(0, 256, (1536, 2048)).astype(np.float32)
+    lying = fb.FourierKernelApprox(255, np.pi / 255, 0, np.array([0.0]), 0.0, 0.0)
+    with pytest.raises(fb.FilterError, match=r"pixel \(0, 0\)"):
+        fb.bilateral_fast(img, fb.make_spatial_gaussian(2.0), lying)
