@@ -120,23 +120,27 @@ __global__ void prep_kernel(const float* __restrict__ src, int2* __restrict__ uf
 // fused path: the same (u, f') on a mirror-padded grid, rows = global rows
 // [out_row0 - W, out_row0 + out_rows + W), columns = global [-W, cols + W)
 // with cols = strips * TW, so every TMA tile of the fused kernel is in bounds.
+// One block row per padded row (blockIdx.y) and image (blockIdx.z), two
+// columns per thread and one 16-byte store: no per-element index divisions.
+// Same per-element arithmetic as the dense prep (bit-identical phases).
 __global__ void prep_padded_kernel(const float* __restrict__ src, int2* __restrict__ uf, Geometry g,
                                    int W, int cols, double turns_scaled, float shift) {
   const int pw = cols + 2 * W, ph = g.out_rows + 2 * W;
-  const long long per = static_cast<long long>(ph) * pw;
-  const long long total = per * g.batch;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long b = i / per;
-    const long long r = i - b * per;
-    const int py = static_cast<int>(r / pw);
-    const int px = static_cast<int>(r - static_cast<long long>(py) * pw);
-    const int gy = mirror_index(g.out_row0 - W + py, g.full_height) - g.src_row0;
-    const int gx = mirror_index(px - W, g.width);
-    const float f = src[b * g.src_bstride + static_cast<long long>(gy) * g.src_pitch + gx];
-    const double fd = static_cast<double>(f) - static_cast<double>(shift);
-    const long long u = __double2ll_rn(fd * turns_scaled);
-    uf[i] = make_int2(static_cast<int>(static_cast<unsigned>(u)), __float_as_int(static_cast<float>(fd)));
+  const int py = blockIdx.y, b = blockIdx.z;
+  const int gy = mirror_index(g.out_row0 - W + py, g.full_height) - g.src_row0;
+  const float* __restrict__ srow = src + b * g.src_bstride + static_cast<long long>(gy) * g.src_pitch;
+  int4* __restrict__ urow = reinterpret_cast<int4*>(uf + (static_cast<long long>(b) * ph + py) * pw);
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; 2 * q < pw; q += gridDim.x * blockDim.x) {
+    int v[4];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int gx = mirror_index(2 * q + e - W, g.width);
+      const double fd = static_cast<double>(srow[gx]) - static_cast<double>(shift);
+      const long long u = __double2ll_rn(fd * turns_scaled);
+      v[2 * e] = static_cast<int>(static_cast<unsigned>(u));
+      v[2 * e + 1] = __float_as_int(static_cast<float>(fd));
+    }
+    urow[q] = make_int4(v[0], v[1], v[2], v[3]);
   }
 }
 
@@ -576,8 +580,9 @@ int fbf_prepare_device(const fbf_geometry* gp, const fbf_filter* f, const float*
   if (P.variant == FBF_VARIANT_FUSED) {
     const int W = f->radius;
     const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
-    const long long n = static_cast<long long>(P.G.batch) * (P.G.out_rows + 2 * W) * (cols + 2 * W);
-    prep_padded_kernel<<<grid_for(n, 256), 256, 0, st>>>(src, P.uf, P.G, W, cols, scale, P.H.shift);
+    const int pairs = (cols + 2 * W) / 2;  // cols is a multiple of 64: even row length
+    const dim3 grid((pairs + 127) / 128, P.G.out_rows + 2 * W, P.G.batch);
+    prep_padded_kernel<<<grid, 128, 0, st>>>(src, P.uf, P.G, W, cols, scale, P.H.shift);
   } else {
     const long long src_px = static_cast<long long>(P.G.batch) * P.G.src_rows * P.G.width;
     prep_kernel<<<grid_for(src_px, 256), 256, 0, st>>>(src, P.uf, P.G, scale, P.H.shift);
