@@ -413,23 +413,19 @@ int harmonic_groups(const fbf_geometry* g, int radius) {
 }
 
 // sum of the nonempty groups' (Q, P) planes -> divide (or -> a dense plane)
+// grid (column blocks, output rows, images): one block row per output row
 __global__ void finish_groups(const p2* __restrict__ pq, int groups, int span, long long plane, int pq_cols,
                               Geometry g, float shift, float q_floor, unsigned long long* bad,
                               float* __restrict__ dst, p2* __restrict__ sum_out) {
-  const long long per_out = static_cast<long long>(g.out_rows) * g.width;
-  const long long total = per_out * g.batch;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long b = i / per_out;
-    const long long r = i - b * per_out;
-    const int yl = static_cast<int>(r / g.width);
-    const int x = static_cast<int>(r % g.width);
-    const long long at = (b * g.out_rows + yl) * pq_cols + x;
+  const int yl = blockIdx.y, b = blockIdx.z;
+  const long long row = (static_cast<long long>(b) * g.out_rows + yl);
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < g.width; x += gridDim.x * blockDim.x) {
+    const long long at = row * pq_cols + x;
     p2 acc = 0ull;
     for (int k = 0; k < groups; ++k)  // fixed order: deterministic
       if (span * (k + 1) / groups > span * k / groups) acc = add2(acc, pq[k * plane + at]);
     if (sum_out) {
-      sum_out[i] = acc;
+      sum_out[row * g.width + x] = acc;
       continue;
     }
     float Q, P;
@@ -441,6 +437,10 @@ __global__ void finish_groups(const p2* __restrict__ pq, int groups, int span, l
     }
     dst[b * g.dst_bstride + static_cast<long long>(yl) * g.dst_pitch + x] = shift + __fdiv_rn(P, Q);
   }
+}
+dim3 rows_grid(const Geometry& g) {
+  return dim3(static_cast<unsigned>((g.width + 255) / 256), static_cast<unsigned>(g.out_rows),
+              static_cast<unsigned>(g.batch));
 }
 
 // Fused: mirror-padded (u, f') image (out_rows + 2W) x (strips*TW + 2W) and a
@@ -616,9 +616,9 @@ int fbf_filter_prepared_device(const fbf_geometry* gp, const fbf_filter* f, floa
       const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
       const long long plane = static_cast<long long>(P.G.batch) * P.G.out_rows * cols;
       const long long out_px = static_cast<long long>(P.G.batch) * P.G.out_rows * P.G.width;
-      finish_groups<<<grid_for(out_px, 256), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), groups,
-                                                          P.H.N + 1, plane, cols, P.G, P.H.shift,
-                                                          P.H.q_floor, d_bad, dst, nullptr);
+      finish_groups<<<rows_grid(P.G), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), groups, P.H.N + 1,
+                                                    plane, cols, P.G, P.H.shift, P.H.q_floor, d_bad, dst,
+                                                    nullptr);
       FBF_CUDA(cudaGetLastError());
     }
     return FBF_OK;
@@ -675,9 +675,9 @@ int fbf_partial_sums_device(const fbf_geometry* gp, const fbf_filter* f, int n_l
     FBF_CUDA(e);
     const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
     const long long plane = static_cast<long long>(P.G.batch) * P.G.out_rows * cols;
-    finish_groups<<<grid_for(out_px, 256), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), groups,
-                                                        n_hi - n_lo, plane, cols, P.G, 0.f, 0.f, nullptr,
-                                                        nullptr, reinterpret_cast<p2*>(pq_out));
+    finish_groups<<<rows_grid(P.G), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), groups, n_hi - n_lo,
+                                                  plane, cols, P.G, 0.f, 0.f, nullptr, nullptr,
+                                                  reinterpret_cast<p2*>(pq_out));
     FBF_CUDA(cudaGetLastError());
     return FBF_OK;
   }
