@@ -758,14 +758,23 @@ std::vector<Chunk> plan_chunks(const fbf_geometry* g, int W, int variant) {
   }
   // one image: K strips cost ~ a + b/K + c*K (b: the copies a strip pipeline
   // hides, c: per-strip prologue rows, launch and tail); fitted on c2 / c4
-  // (profiles/r01_notes.md): K ~ sqrt(b/c) ~ sqrt(pixels / 0.45 M), at most 6
+  // (profiles/r01_notes.md): K ~ sqrt(b/c) ~ sqrt(pixels / 0.45 M), at most 4
   int best = static_cast<int>(std::lround(std::sqrt(px / 0.45e6)));
-  best = std::max(1, std::min(best, 6));
+  best = std::max(1, std::min(best, 4));
   if (const char* force = getenv("FBF_HOST_CHUNKS")) best = std::max(1, atoi(force));  // experiments
   while (best > 1 && g->out_rows / best < 4 * W + 16) --best;
+  // the first strip's H2D and the last strip's D2H are not hidden: those two
+  // strips get 20 % of a middle strip's rows (measured: c2 K=3 2553 -> 2730,
+  // c4 K=4 1637 -> 1707 e2e Mpixel/s; FBF_HOST_EDGE overrides, experiments)
+  const long long e = best >= 3 ? (getenv("FBF_HOST_EDGE") ? atoi(getenv("FBF_HOST_EDGE")) : 20) : 100;
+  const long long wsum = 2 * e + 100LL * (best - 2);
+  auto cut = [&](int i) {  // cumulative weight of strips [0, i)
+    const long long w = i == 0 ? 0 : i == best ? wsum : e + 100LL * (i - 1);
+    return g->out_row0 + static_cast<int>(g->out_rows * w / wsum) / 16 * 16;
+  };
   for (int i = 0; i < best; ++i) {
-    int o0 = g->out_row0 + (g->out_rows * i / best) / 16 * 16;
-    int o1 = i + 1 == best ? g->out_row0 + g->out_rows : g->out_row0 + (g->out_rows * (i + 1) / best) / 16 * 16;
+    int o0 = cut(i);
+    int o1 = i + 1 == best ? g->out_row0 + g->out_rows : cut(i + 1);
     if (i == 0) o0 = g->out_row0;
     if (o1 <= o0) continue;
     const int s0 = std::max(g->src_row0, std::max(0, o0 - W));
