@@ -747,10 +747,15 @@ std::vector<Chunk> plan_chunks(const fbf_geometry* g, int W, int variant) {
     c.push_back({0, g->batch, g->out_row0, g->out_row0 + g->out_rows, g->src_row0, g->src_row0 + g->src_rows});
     return c;
   }
-  if (g->batch >= 2) {  // whole images per chunk
+  if (g->batch >= 2) {  // whole images per chunk; the first and last chunk at 20 % weight
     const int k = std::min(g->batch, 8);
+    const long long e = k >= 3 ? 20 : 100, wsum = 2 * e + 100LL * (k - 2);
+    auto cut = [&](int i) {
+      const long long w = i == 0 ? 0 : i == k ? wsum : e + 100LL * (i - 1);
+      return static_cast<int>(g->batch * w / wsum);
+    };
     for (int i = 0; i < k; ++i) {
-      const int b0 = g->batch * i / k, b1 = g->batch * (i + 1) / k;
+      const int b0 = cut(i), b1 = cut(i + 1);
       if (b1 > b0)
         c.push_back({b0, b1 - b0, g->out_row0, g->out_row0 + g->out_rows, g->src_row0, g->src_row0 + g->src_rows});
     }
