@@ -104,22 +104,16 @@ struct Lanes {
   static_assert(C::G % NWARP == 0, "rows per warp");
 };
 
-// TMA loads of one step: the padded (u, f') rows [a, a+G) x columns
-// [x0-W, x0+TW+W) into stage, and the running (Q, P) of output rows [o, o+G)
-// into pqs.  Issued by thread 0 only; rows past the image are zero-filled
-// and never consumed.
+// TMA load of the padded (u, f') rows [a, a+G) x columns [x0-W, x0+TW+W)
+// into stage (the bootstrap of a unit); the step loop issues it together with
+// the running (Q, P) rows of the step on one barrier phase.  Issued by thread
+// 0 only; rows past the image are zero-filled and never consumed.
 template <class C>
 __device__ __forceinline__ void tma_uf(const FusedArgs& A, int2* stage, uint64_t* bar, const Unit& u,
                                        int a) {
   mbar_expect_tx(bar, static_cast<unsigned>(C::G * C::MW * 8));
   tma_load_3d(stage, &A.tm_uf, bar, u.x0, a - A.g.out_row0 + C::W, u.b);
 }
-template <class C>
-__device__ __forceinline__ void tma_pq(const FusedArgs& A, p2* pqs, uint64_t* bar, const Unit& u, int o) {
-  mbar_expect_tx(bar, static_cast<unsigned>(C::G * C::TW * 8));
-  tma_load_3d(pqs, &A.tm_pq, bar, u.x0, o - A.g.out_row0, static_cast<int>(blockIdx.y) * A.g.batch + u.b);
-}
-
 // Modulation of one step, sliced into RPW*NJ independent elements per thread.
 // Straight-line code: every slot is computed (clamped reads) and only the
 // stores are predicated, so the element chains interleave freely with other
@@ -433,15 +427,13 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
   float* CS = reinterpret_cast<float*>(smem + C::OFF_CS);
   p2* pqs = reinterpret_cast<p2*>(smem + C::OFF_PQ);
   uint64_t* bar_uf = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* bar_pq = bar_uf + 1;
   const bool leader = threadIdx.x == 0;
   if (leader) {
     mbar_init(bar_uf, 1);
-    mbar_init(bar_pq, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  unsigned ph_uf = 0, ph_pq = 0;  // phase parity of the next completion of each barrier
+  unsigned ph_uf = 0;  // phase parity of the next completion of the copy barrier
   PhaseClock clk;
   clk.start();
 
@@ -504,20 +496,21 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
         clk.mark(0);
         __syncthreads();  // S1: M holds this step; the previous column pass is done; stage free
         clk.mark(1);
-        if (leader) {
+        // the next step's (u, f') rows and this step's (Q, P) complete on one
+        // barrier phase (one wait instead of two)
+        if (leader && (more || want_pq)) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          if (more) tma_uf<C>(A, stage, bar_uf, u, a2);
-          if (want_pq) tma_pq<C>(A, pqs, bar_pq, u, o);
+          mbar_expect_tx(bar_uf, (more ? C::G * C::MW * 8u : 0u) + (want_pq ? C::G * C::TW * 8u : 0u));
+          if (more) tma_load_3d(stage, &A.tm_uf, bar_uf, u.x0, a2 - A.g.out_row0 + C::W, u.b);
+          if (want_pq)
+            tma_load_3d(pqs, &A.tm_pq, bar_uf, u.x0, o - A.g.out_row0,
+                        static_cast<int>(blockIdx.y) * A.g.batch + u.b);
         }
         row_pass<C>(A, M, R, CS, a, rows, base);
         clk.mark(2);
-        if (more) {
+        if (more || want_pq) {
           mbar_wait(bar_uf, ph_uf);
           ph_uf ^= 1u;
-        }
-        if (want_pq) {
-          mbar_wait(bar_pq, ph_pq);
-          ph_pq ^= 1u;
         }
         clk.mark(3);
         __syncthreads();  // S2: ring rows visible, next (u, f') and this step's (Q, P) landed, M free
