@@ -92,18 +92,6 @@ __device__ __forceinline__ void step_rows(const Unit& u, int s, int& a, int& row
   }
 }
 
-// Warp-row mapping shared by the prefetch and the modulation: warp w owns the
-// step rows g = w, w + NWARP, ...; lane l owns the columns j = l + 32 i of a
-// row.  The mirrored global column of each owned j is computed once per work
-// unit (colofs), so the per-element cost is an add and the copy itself.
-template <class C>
-struct Lanes {
-  static constexpr int NWARP = C::NT / 32;
-  static constexpr int RPW = C::G / NWARP;      // rows per warp per step
-  static constexpr int NJ = (C::MW + 31) / 32;  // column slots per lane
-  static_assert(C::G % NWARP == 0, "rows per warp");
-};
-
 // TMA load of the padded (u, f') rows [a, a+G) x columns [x0-W, x0+TW+W)
 // into stage (the bootstrap of a unit); the step loop issues it together with
 // the running (Q, P) rows of the step on one barrier phase.  Issued by thread
@@ -121,57 +109,54 @@ __device__ __forceinline__ void tma_uf(const FusedArgs& A, int2* stage, uint64_t
 // data and are never consumed).
 template <class C>
 struct ModNext {
-  static constexpr int ELEMS = Lanes<C>::RPW * Lanes<C>::NJ;
+  // Two lane mappings of the step's G x MW elements (both: consecutive lanes
+  // on consecutive columns, conflict-free stage reads and M writes):
+  //  * warp rows: warp w owns rows w, w + NWARP, ...; lane l columns l + 32 i
+  //    (slots past a row's end are computed and dropped);
+  //  * linear: element e = tid + NT * k in row-major order (no dropped slots,
+  //    one division by MW per element).
+  // Linear where it saves elements (c1 / c3 / c5 +1-2 %), else warp rows.
+  static constexpr int TOTAL = C::G * C::MW;
+  static constexpr int NWARP = C::NT / 32;
+  static constexpr int NJ = (C::MW + 31) / 32;
+  static constexpr int ELEMS_ROWS = (C::G / NWARP) * NJ;
+  static constexpr int ELEMS_LIN = (TOTAL + C::NT - 1) / C::NT;
+  static constexpr bool LINEAR = ELEMS_LIN < ELEMS_ROWS;
+  static constexpr int ELEMS = LINEAR ? ELEMS_LIN : ELEMS_ROWS;  // per thread
+  static_assert(C::G % NWARP == 0, "rows per warp");
+  static_assert(C::MP == C::MW + 1, "M pitch: one pad column (MW is even)");
   const int2* stage;
   p2* M;  // plane A; plane B follows at + G * MP
   uint32_t n;
 
-  // k must be a constant after unrolling (all callers sit in unrolled loops)
-  __device__ __forceinline__ void element(int k) const { element_at(k, stage, M, n); }
-  // restrict-qualified form: callers that interleave the elements with other
-  // shared-memory traffic pass their pointers here, so the compiler may move
-  // the element chains past the other loads and stores
-  static __device__ __forceinline__ void element_at(int k, const int2* __restrict__ stage, p2* __restrict__ M,
-                                                    uint32_t n) {
-    using L = Lanes<C>;
-    const int r = k / L::NJ, i = k % L::NJ;
-    const bool full = (C::MW % 32 == 0) || (i + 1 < L::NJ);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = warp + r * L::NWARP;
-    const int j = lane + 32 * i;
-    const int jc = full ? j : min(j, C::MW - 1);
-    const int2 v = stage[g * C::MW + jc];
-    float c, s;
-    sincos_turns(n * static_cast<uint32_t>(v.x), c, s);
-    const float fp = __int_as_float(v.y);
-    if (full || j < C::MW) {
-      M[g * C::MP + j] = pk(c, c * fp);
-      M[(C::G + g) * C::MP + j] = pk(s, s * fp);
-    }
-  }
-  // elements K0 .. K0+NB-1 with every stage of the chain issued for all NB
-  // before the next: NB independent chains in flight (the compiler tends to
-  // run single elements back to back, exposing the ~20-deep dependency chain)
-  // (k0 must be a constant after unrolling)
+  // elements k0 .. k0+NB-1 of this thread with every stage of the chain issued
+  // for all NB before the next: NB independent chains in flight (the compiler
+  // tends to run single elements back to back, exposing the ~20-deep
+  // dependency chain).  k0 must be a constant after unrolling.
   template <int NB>
   static __device__ __forceinline__ void elements(int k0, const int2* __restrict__ stage, p2* __restrict__ M,
                                                   uint32_t n) {
-    using L = Lanes<C>;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int2 v[NB];
     int off[NB];
     bool ok[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int k = k0 + b;
-      const int r = k / L::NJ, i = k % L::NJ;
-      const bool full = (C::MW % 32 == 0) || (i + 1 < L::NJ);
-      const int g = warp + r * L::NWARP;
-      const int j = lane + 32 * i;
-      const int jc = full ? j : min(j, C::MW - 1);
-      ok[b] = full || j < C::MW;
-      off[b] = g * C::MP + j;
-      v[b] = stage[g * C::MW + jc];
+      if constexpr (LINEAR) {
+        const int e = static_cast<int>(threadIdx.x) + C::NT * k;
+        ok[b] = TOTAL % C::NT == 0 || e < TOTAL;
+        const int ec = (TOTAL % C::NT == 0) ? e : min(e, TOTAL - 1);
+        off[b] = ec + ec / C::MW;  // g * MP + j with MP = MW + 1
+        v[b] = stage[ec];
+      } else {
+        const int r = k / NJ, i = k % NJ;
+        const bool full = (C::MW % 32 == 0) || (i + 1 < NJ);
+        const int g = static_cast<int>(threadIdx.x >> 5) + r * NWARP;
+        const int j = static_cast<int>(threadIdx.x & 31) + 32 * i;
+        ok[b] = full || j < C::MW;
+        off[b] = g * C::MP + j;
+        v[b] = stage[g * C::MW + (full ? j : min(j, C::MW - 1))];
+      }
     }
     float c[NB], s[NB];
     sincos_turns_n<NB>(n, v, c, s);
@@ -184,17 +169,23 @@ struct ModNext {
       }
     }
   }
+  // batch b of ceil(ELEMS / 4): four elements, the last batch the remainder
+  static constexpr int NBATCH = (ELEMS + 3) / 4;
+  static __device__ __forceinline__ void batch(int b, const int2* __restrict__ stage, p2* __restrict__ M,
+                                               uint32_t n) {
+    if (4 * b + 4 <= ELEMS)
+      elements<4>(4 * b, stage, M, n);
+    else
+      elements<(ELEMS % 4 ? ELEMS % 4 : 4)>(4 * b, stage, M, n);
+  }
 };
 
 template <class C>
 __device__ __forceinline__ void modulate_rows(const int2* __restrict__ stage, p2* __restrict__ M,
                                               int rows, uint32_t n) {
   (void)rows;
-  constexpr int E = ModNext<C>::ELEMS;
 #pragma unroll
-  for (int k = 0; k + 4 <= E; k += 4) ModNext<C>::template elements<4>(k, stage, M, n);
-#pragma unroll
-  for (int k = E - E % 4; k < E; ++k) ModNext<C>::element_at(k, stage, M, n);
+  for (int b = 0; b < ModNext<C>::NBATCH; ++b) ModNext<C>::batch(b, stage, M, n);
 }
 
 // FBF_PHASE_PROF builds: thread 0 (and 128) of every CTA sums the cycles of
@@ -305,14 +296,11 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
   const p2* __restrict__ Rh = R + h * C::RING * C::RP + x;
   const int s0 = (r0 - C::W - base) % C::RING;
   constexpr int TAPS_IN = C::KC + 2 * C::W;
-  constexpr int ELEMS = ModNext<C>::ELEMS;
-  static_assert(ELEMS % 4 == 0, "modulation batches of 4");
-  constexpr int NBATCH = ELEMS / 4;
+  constexpr int NBATCH = ModNext<C>::NBATCH;
   constexpr int STRIDE = TAPS_IN / NBATCH > 0 ? TAPS_IN / NBATCH : 1;
-  // one batch of 4 modulation elements of the next step per STRIDE taps
+  // one batch of (up to) 4 modulation elements of the next step per STRIDE taps
   auto batch = [&](int m) {
-    if (m % STRIDE == 0 && m / STRIDE < NBATCH)
-      ModNext<C>::template elements<4>(4 * (m / STRIDE), next.stage, next.M, next.n);
+    if (m % STRIDE == 0 && m / STRIDE < NBATCH) ModNext<C>::batch(m / STRIDE, next.stage, next.M, next.n);
   };
   auto ring = [&](int m) {
     int s = s0 + m;
@@ -352,7 +340,7 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
   }
 #pragma unroll
   for (int b = TAPS_IN / STRIDE + (TAPS_IN % STRIDE ? 1 : 0); b < NBATCH; ++b)
-    ModNext<C>::template elements<4>(4 * b, next.stage, next.M, next.n);
+    ModNext<C>::batch(b, next.stage, next.M, next.n);
   clk.mark(5);
   // (q, p) = c (Gc, Fc) + s (Gs, Fs)   [bilateral.hpp:138-144, real form]:
   // this lane's half of every row, then swap halves with the partner lane
