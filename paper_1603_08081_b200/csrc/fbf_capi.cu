@@ -848,11 +848,15 @@ int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const fl
       cudaStream_t st = sts[k & 1];
       // H2D: this chunk's images, or the source rows no earlier strip has copied
       const int r0 = g->batch >= 2 || K == 1 ? c.s0 : std::max(c.s0, copied_hi);
-      for (int b = c.b0; b < c.b0 + c.nb && r0 < c.s1; ++b) {
+      // images stacked without gaps (whole rows, bstride = rows * pitch): one 2-D copy
+      const bool src_stacked = r0 == g->src_row0 && c.s1 == g->src_row0 + g->src_rows &&
+                               g->src_bstride == static_cast<long long>(g->src_rows) * g->src_pitch;
+      for (int b = c.b0; b < c.b0 + c.nb && r0 < c.s1; b += src_stacked ? c.nb : 1) {
         e = cudaMemcpy2DAsync(d_src + b * sb + static_cast<long long>(r0 - g->src_row0) * g->width,
                               g->width * sizeof(float),
                               src + b * g->src_bstride + static_cast<long long>(r0 - g->src_row0) * g->src_pitch,
-                              g->src_pitch * sizeof(float), g->width * sizeof(float), c.s1 - r0,
+                              g->src_pitch * sizeof(float), g->width * sizeof(float),
+                              src_stacked ? static_cast<size_t>(c.nb) * g->src_rows : c.s1 - r0,
                               cudaMemcpyHostToDevice, st);
         if (e != cudaSuccess) break;
       }
@@ -869,11 +873,14 @@ int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const fl
                                       d_dst + c.b0 * db + static_cast<long long>(c.o0 - g->out_row0) * g->width,
                                       ws0 + (k & 1) * (nws > 1 ? ws_bytes : 0), ws_bytes, d_bad + k, v, st);
       if (out != FBF_OK) break;
-      for (int b = c.b0; b < c.b0 + c.nb; ++b) {
+      const bool dst_stacked = c.o0 == g->out_row0 && c.o1 == g->out_row0 + g->out_rows &&
+                               g->dst_bstride == static_cast<long long>(g->out_rows) * g->dst_pitch;
+      for (int b = c.b0; b < c.b0 + c.nb; b += dst_stacked ? c.nb : 1) {
         e = cudaMemcpy2DAsync(dst + b * g->dst_bstride + static_cast<long long>(c.o0 - g->out_row0) * g->dst_pitch,
                               g->dst_pitch * sizeof(float),
                               d_dst + b * db + static_cast<long long>(c.o0 - g->out_row0) * g->width,
-                              g->width * sizeof(float), g->width * sizeof(float), c.o1 - c.o0,
+                              g->width * sizeof(float), g->width * sizeof(float),
+                              dst_stacked ? static_cast<size_t>(c.nb) * g->out_rows : c.o1 - c.o0,
                               cudaMemcpyDeviceToHost, st);
         if (e != cudaSuccess) break;
       }

@@ -17,10 +17,6 @@ import torch  # noqa: E402
 import paper_1603_08081_b200 as fb  # noqa: E402
 from paper_1603_08081_b200.configs import CONFIGS, approx_of, image_of, spatial_of  # noqa: E402
 
-WS_PROD = ["loop top", "wait R slot empty", "issue copies", "row pass + next mod", "copy waits + arrive",
-           "producer barrier", "-", "-"]
-WS_CONS = ["loop top", "wait R slot full", "-", "step body", "fence + arrive", "shift + next",
-           "-", "-"]
 NAMES = ["loop top", "S1 wait", "row pass", "TMA waits", "S2 wait", "col FIR + next mod", "prologue mod", "demod + stores"]
 
 
@@ -41,24 +37,14 @@ def main(name):
                                  bad.data_ptr())
         torch.cuda.synchronize()
         fn(buf)
-    kernel = os.environ.get("FBF_FUSED_CFG", "ws")
-    names = WS_PROD if kernel[0] not in "sb" else NAMES
     steps = buf[8]
-    print(f"{name} ({kernel}): {steps} steps (thread 0 of every CTA), cycles per step:")
+    print(f"{name}: {steps} steps (thread 0 of every CTA), cycles per step:")
     tot = 0
     for i in range(8):
         v = buf[i] / max(steps, 1)
         tot += v
-        print(f"  {names[i]:<22} {v:8.0f}")
+        print(f"  {NAMES[i]:<22} {v:8.0f}")
     print(f"  {'total':<22} {tot:8.0f}")
-    if buf[17]:
-        print(f"  consumer (thread 128), {buf[17]} steps:")
-        tot = 0
-        for i in range(8):
-            v = buf[9 + i] / buf[17]
-            tot += v
-            print(f"  {WS_CONS[i]:<22} {v:8.0f}")
-        print(f"  {'total':<22} {tot:8.0f}")
 
 
 if __name__ == "__main__":
