@@ -562,14 +562,25 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
                      static_cast<unsigned long long>(a.g.out_rows),
                      static_cast<unsigned long long>(a.g.batch) * a.groups, C::TW, C::G);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(fused_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(C::smem_bytes));
+  // per device, once: the smem opt-in and the resident CTAs per SM (host calls
+  // that would otherwise sit on every launch's critical path)
+  struct DevInfo {
+    int dev = -1, sms = 0, occ = 0;
+  };
+  thread_local DevInfo info;
+  int dev = 0;
+  e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  int dev = 0, sms = 0, occ = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel<C>, C::NT, C::smem_bytes);
-  if (occ < 1) occ = 1;
+  if (info.dev != dev) {
+    e = cudaFuncSetAttribute(fused_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(C::smem_bytes));
+    if (e != cudaSuccess) return e;
+    cudaDeviceGetAttribute(&info.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ, fused_kernel<C>, C::NT, C::smem_bytes);
+    if (info.occ < 1) info.occ = 1;
+    info.dev = dev;
+  }
+  const int sms = info.sms, occ = info.occ;
   // one wave in total: the harmonic groups share the SMs
   long long grid = (static_cast<long long>(sms) * occ + a.groups - 1) / a.groups;
   // keep at least ~2W+G rows per CTA so the per-unit prologue stays amortised
