@@ -21,7 +21,8 @@ Image bilateral_exact(const Image& image, const SpatialKernel& spatial, const Ra
 
 /// Shiftable Fourier-kernel bilateral filter (Algorithm 1), on the GPU.
 /// invalid_argument: empty image, or approx.max_pointwise_error >= spatial.w0,
-/// or the recursive backend.  runtime_error: "... denominator collapsed at pixel (x, y)".
+/// runtime_error: "... denominator collapsed at pixel (x, y)".  The recursive
+/// backend (Gaussian windows with sigma >= 2) runs the fp64 IIR path on the GPU.
 Image bilateral_fast(const Image& image, const SpatialKernel& spatial,
                      const FourierKernelApprox& approx,
                      ConvolutionBackend backend = ConvolutionBackend::direct);

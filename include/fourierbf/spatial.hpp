@@ -13,7 +13,7 @@ enum class SpatialKind { gaussian, box };
 
 enum class ConvolutionBackend {
     direct,     ///< separable FIR (the B200 path)
-    recursive,  ///< IIR Gaussian: not provided by this build (throws invalid_argument)
+    recursive,  ///< third-order IIR Gaussian for Gaussian windows with sigma >= 2 (GPU, fp64)
 };
 
 /// Separable symmetric window on [-W, W]^2 with a unit-sum 1-D profile.
@@ -38,7 +38,7 @@ SpatialKernel make_spatial_box(int radius);
 using Plane = Image;
 
 /// Mirror-boundary separable convolution on the GPU; invalid_argument on an
-/// empty plane or on the recursive backend.
+/// empty plane.  The recursive backend (Gaussian, sigma >= 2) runs the IIR.
 Plane convolve(const Plane& plane, const SpatialKernel& kernel,
                ConvolutionBackend backend = ConvolutionBackend::direct);
 

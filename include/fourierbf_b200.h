@@ -39,6 +39,12 @@ extern "C" {
 
 #define FBF_VARIANT_FUSED 0 /* one fused kernel (default)                        */
 #define FBF_VARIANT_NAIVE 1 /* multi-kernel, HBM-resident planes (comparison)    */
+/* ConvolutionBackend::recursive (spatial.hpp:98-112, recursive_gaussian.hpp):
+ * the IIR Gaussian of the filter's sigma_s, fp64, whole images; like the
+ * reference it applies to Gaussian windows with sigma_s >= 2 and falls back to
+ * the direct (fused) path otherwise.  Through fbf_bilateral_fast_device and the
+ * host entry points (not the prepare / filter_prepared split). */
+#define FBF_VARIANT_RECURSIVE 2
 
 /* Where the pixels are.  The global image is width x height.  A buffer holds
  * rows [src_row0, src_row0 + src_rows) of each of `batch` images (row strips
@@ -64,6 +70,7 @@ typedef struct fbf_filter {
   double omega;           /* pi / T                                         */
   double max_pointwise_error; /* epsilon of the fit                         */
   int check_epsilon;      /* 1: enforce eps < w0 like bilateral.hpp:114-118 */
+  double sigma_s;         /* spatial sigma (FBF_VARIANT_RECURSIVE); 0 if unknown */
 } fbf_filter;
 
 const char* fbf_last_error(void);
@@ -125,6 +132,9 @@ int fbf_convolve_device(int width, int height, const double* profile, int radius
                         void* stream);
 int fbf_convolve_host_f64(int width, int height, const double* profile, int radius,
                           const double* src, double* dst);
+/* convolve with the recursive backend: the IIR Gaussian of sigma (fp64; the
+ * caller applies the reference's rule: Gaussian windows with sigma >= 2). */
+int fbf_convolve_recursive_host_f64(int width, int height, double sigma, const double* src, double* dst);
 
 /* bilateral_exact (bilateral.hpp:78-102) on the device in fp64: the O(W^2)
  * brute-force filter, for checking the paper's bound at full image sizes.

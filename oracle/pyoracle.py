@@ -186,7 +186,10 @@ class Reference:
         L.ref_cli_run.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_double, ctypes.c_double,
                                   ctypes.c_double, ctypes.c_int, ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
                                   ctypes.c_char_p, ctypes.c_int, ctypes.c_char_p, ctypes.c_size_t,
-                                  ctypes.c_char_p, ctypes.c_size_t]
+                                  ctypes.c_char_p, ctypes.c_size_t, ctypes.c_int]
+        L.ref_convolve_recursive.argtypes = [_D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_double]
+        L.ref_bilateral_fast_recursive.argtypes = [_D, ctypes.c_int, ctypes.c_int, ctypes.c_double, _D, ctypes.c_int,
+                                                   ctypes.c_int, ctypes.c_double, _D]
         L.ref_encode_pgm.restype = ctypes.c_long
         L.ref_encode_pgm.argtypes = [_D, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_size_t]
         self.L = L
@@ -276,11 +279,30 @@ class Reference:
         return buf.raw[:n]
 
     def cli_run(self, input_path, output_path="", sigma_s=1.0, sigma_r=30.0, epsilon=1e-3, family=0, table="",
-                spatial=0, compare_exact=False, report="", bench=False):
+                spatial=0, compare_exact=False, report="", bench=False, backend=0):
         """cli.hpp run() -> (rc, stdout text, stderr text)"""
         out = ctypes.create_string_buffer(1 << 16)
         err = ctypes.create_string_buffer(1 << 12)
         enc = lambda v: v.encode() if v else None  # noqa: E731
         rc = self.L.ref_cli_run(enc(input_path), enc(output_path), sigma_s, sigma_r, epsilon, family, enc(table),
-                                spatial, int(compare_exact), enc(report), int(bench), out, len(out), err, len(err))
+                                spatial, int(compare_exact), enc(report), int(bench), out, len(out), err, len(err),
+                                backend)
         return rc, out.value.decode(), err.value.decode()
+
+    def convolve_recursive(self, img, sigma):
+        """convolve(..., ConvolutionBackend::recursive) on a whole image"""
+        a = _f64(img)
+        out = np.empty_like(a)
+        if self.L.ref_convolve_recursive(_dp(a), _dp(out), a.shape[1], a.shape[0], sigma):
+            raise ValueError(self.last_error())
+        return out
+
+    def bilateral_fast_recursive(self, img, sigma, d, T, max_err):
+        """bilateral_fast(..., ConvolutionBackend::recursive) on a whole image, Gaussian window of sigma"""
+        a = _f64(img)
+        out = np.empty_like(a)
+        dd = _f64(d)
+        if self.L.ref_bilateral_fast_recursive(_dp(a), a.shape[1], a.shape[0], sigma, _dp(dd), len(dd) - 1, T, max_err,
+                                               _dp(out)):
+            raise ValueError(self.last_error())
+        return out

@@ -272,8 +272,9 @@ long ref_encode_pgm(const double* values, int w, int h, char* out, size_t cap) {
 // run()'s code; its stdout / stderr text is copied into out / err (cap bytes).
 int ref_cli_run(const char* input, const char* output, double sigma_s, double sigma_r, double epsilon,
                 int family, const char* table, int spatial, int compare_exact, const char* report, int bench,
-                char* out, size_t out_cap, char* err, size_t err_cap) {
+                char* out, size_t out_cap, char* err, size_t err_cap, int backend) {
     fb::CliOptions opt;
+    opt.backend = backend == 1 ? fb::ConvolutionBackend::recursive : fb::ConvolutionBackend::direct;
     opt.input_path = input ? input : "";
     opt.output_path = output ? output : "";
     opt.sigma_s = sigma_s;
@@ -294,6 +295,39 @@ int ref_cli_run(const char* input, const char* output, double sigma_s, double si
     std::memcpy(out, so.data(), std::min(out_cap - 1, so.size()));
     std::memcpy(err, se.data(), std::min(err_cap - 1, se.size()));
     return rc;
+}
+
+// convolve / bilateral_fast with ConvolutionBackend::recursive (the IIR Gaussian,
+// recursive_gaussian.hpp) on a whole w*h image; Gaussian window of sigma.
+int ref_convolve_recursive(const double* in, double* out, int w, int h, double sigma) {
+    try {
+        const fb::Plane p = fb::convolve(image_of(in, w, h, 0, h), fb::make_spatial_gaussian(sigma),
+                                         fb::ConvolutionBackend::recursive);
+        std::copy(p.values.begin(), p.values.end(), out);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+int ref_bilateral_fast_recursive(const double* img, int w, int h, double sigma, const double* d, int N, int T,
+                                 double max_err, double* out) {
+    try {
+        fb::FourierKernelApprox a;
+        a.T = T;
+        a.omega = std::numbers::pi / T;
+        a.N = N;
+        a.d.assign(d, d + N + 1);
+        a.max_pointwise_error = max_err;
+        const fb::Image res = fb::bilateral_fast(image_of(img, w, h, 0, h), fb::make_spatial_gaussian(sigma), a,
+                                                 fb::ConvolutionBackend::recursive);
+        std::copy(res.values.begin(), res.values.end(), out);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
 }
 
 }  // extern "C"

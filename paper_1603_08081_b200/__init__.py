@@ -24,8 +24,9 @@ LIB_PATH = os.environ.get("FBF_LIBRARY") or os.path.join(_HERE, "_lib", "libfour
 FBF_OK, FBF_EINVAL, FBF_EANOMALY, FBF_ECUDA, FBF_EUNSUPPORTED = 0, 1, 2, 3, 4
 SPATIAL_GAUSSIAN, SPATIAL_BOX = 0, 1
 RANGE_GAUSSIAN, RANGE_EXPONENTIAL = 0, 1
-VARIANT_FUSED, VARIANT_NAIVE = 0, 1
-_VARIANTS = {"fused": VARIANT_FUSED, "naive": VARIANT_NAIVE}
+VARIANT_FUSED, VARIANT_NAIVE, VARIANT_RECURSIVE = 0, 1, 2
+# "recursive" = ConvolutionBackend::recursive (IIR Gaussian, fp64; Gaussian windows with sigma >= 2)
+_VARIANTS = {"fused": VARIANT_FUSED, "naive": VARIANT_NAIVE, "recursive": VARIANT_RECURSIVE}
 
 
 class Geometry(ctypes.Structure):
@@ -45,6 +46,7 @@ class Filter(ctypes.Structure):
         ("N", ctypes.c_int), ("d", ctypes.POINTER(ctypes.c_double)),
         ("omega", ctypes.c_double), ("max_pointwise_error", ctypes.c_double),
         ("check_epsilon", ctypes.c_int),
+        ("sigma_s", ctypes.c_double),
     ]
 
 
@@ -76,6 +78,7 @@ SIGNATURES = {
     "fbf_convolve_device": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _D, ctypes.c_int, _P, _P, _P,
                                            ctypes.c_size_t, _P]),
     "fbf_convolve_host_f64": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _D, ctypes.c_int, _D, _D]),
+    "fbf_convolve_recursive_host_f64": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_double, _D, _D]),
     "fbf_spatial_gaussian": (ctypes.c_int, [ctypes.c_double, _D, _I, _D]),
     "fbf_spatial_box": (ctypes.c_int, [ctypes.c_int, _D, _D]),
     "fbf_range_eval": (ctypes.c_double, [ctypes.c_int, ctypes.c_double, ctypes.c_double]),
@@ -244,7 +247,7 @@ def _filter_struct(spatial: SpatialKernel, approx: FourierKernelApprox, check_ep
     prof = np.ascontiguousarray(spatial.profile, dtype=np.float64)
     d = np.ascontiguousarray(approx.d, dtype=np.float64)
     f = Filter(spatial.kind, spatial.radius, _dp(prof), spatial.w0, approx.N, _dp(d), approx.omega,
-               approx.max_pointwise_error, 1 if check_epsilon else 0)
+               approx.max_pointwise_error, 1 if check_epsilon else 0, spatial.sigma_s)
     f._keep = (prof, d)  # keep the buffers alive with the struct
     return f
 
@@ -376,12 +379,16 @@ def bilateral_exact_gpu(image: np.ndarray, spatial: SpatialKernel, family: int, 
     return dst.cpu().numpy()
 
 
-def convolve(plane: np.ndarray, spatial: SpatialKernel) -> np.ndarray:
-    """spatial.hpp:98-112 (direct backend) on the GPU."""
+def convolve(plane: np.ndarray, spatial: SpatialKernel, backend: str = "direct") -> np.ndarray:
+    """spatial.hpp:98-112 on the GPU; backend "recursive" runs the IIR Gaussian
+    for Gaussian windows with sigma >= 2 and the direct path otherwise, like the reference."""
     p = np.ascontiguousarray(plane, dtype=np.float64)
     if p.size == 0:
         raise ValueError("convolve: empty plane")
     out = np.empty_like(p)
+    if backend == "recursive" and spatial.kind == SPATIAL_GAUSSIAN and spatial.sigma_s >= 2.0:
+        _check(lib.fbf_convolve_recursive_host_f64(p.shape[1], p.shape[0], spatial.sigma_s, _dp(p), _dp(out)))
+        return out
     prof = np.ascontiguousarray(spatial.profile, dtype=np.float64)
     _check(lib.fbf_convolve_host_f64(p.shape[1], p.shape[0], _dp(prof), spatial.radius, _dp(p), _dp(out)))
     return out

@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "fbf_common.h"
 #include "fbf_device.cuh"
 #include "fbf_params.h"
 #include "fourierbf_b200.h"
@@ -23,25 +24,25 @@ cudaError_t launch_fused(const FusedArgs& a, cudaStream_t st, int* grid_out);
 using namespace fbf;
 
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
 
+namespace fbf {
 int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
-
 int cuda_fail(cudaError_t e, const char* where) {
   return fail(FBF_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
+// recursive (IIR) backend, fbf_iir.cu
+size_t iir_workspace_bytes(const fbf_geometry* g, int radius);
+template <class Tin, class Tout>
+int iir_bilateral(const fbf_geometry* g, const fbf_filter* f, const Tin* src, Tout* dst, void* ws, size_t ws_bytes,
+                  unsigned long long* d_bad, cudaStream_t st);
+}  // namespace fbf
 
-#define FBF_CUDA(call)                                  \
-  do {                                                  \
-    cudaError_t e_ = (call);                            \
-    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
-  } while (0)
-
-size_t align256(size_t n) { return (n + 255) & ~size_t(255); }
+namespace {
 
 // The synchronous host entry points keep one stream and one grow-only device
 // buffer per calling thread (and device): no allocation, stream creation or
@@ -319,6 +320,10 @@ int check_geometry(const fbf_geometry* g) {
   return FBF_OK;
 }
 
+// spatial.hpp:102-104: the recursive backend replaces the FIR for Gaussian
+// windows with sigma >= 2 only
+bool uses_iir(const fbf_filter* f) { return f->kind == FBF_SPATIAL_GAUSSIAN && f->sigma_s >= 2.0; }
+
 int check_filter(const fbf_filter* f) {
   if (!f || !f->profile || !f->d) return fail(FBF_EINVAL, "bilateral_fast: null filter");
   if (f->radius < 1 || f->radius > kMaxW)
@@ -494,6 +499,8 @@ void fbf_geometry_whole(fbf_geometry* g, int width, int height, int batch) {
 
 size_t fbf_workspace_bytes(const fbf_geometry* g, int radius, int variant) {
   if (check_geometry(g) != FBF_OK || radius < 1 || radius > kMaxW) return 0;
+  if (variant == FBF_VARIANT_RECURSIVE)  // the IIR path, or the direct path it falls back to
+    return std::max(iir_workspace_bytes(g, radius), fbf_workspace_bytes(g, radius, FBF_VARIANT_FUSED));
   if (variant == FBF_VARIANT_FUSED) {
     const bool g_ok = fused_supported(radius, false), b_ok = fused_supported(radius, true);
     if (!g_ok && !b_ok) variant = FBF_VARIANT_NAIVE;
@@ -548,6 +555,12 @@ int prepare_common(const fbf_geometry* gp, const fbf_filter* f, void* workspace,
   if (rc) return rc;
   if ((rc = check_filter(f))) return rc;
   if ((rc = check_halo(gp, f->radius))) return rc;
+  if (variant == FBF_VARIANT_RECURSIVE) {
+    if (uses_iir(f))
+      return fail(FBF_EUNSUPPORTED,
+                  "bilateral_fast: the recursive backend runs through fbf_bilateral_fast_device / _host only");
+    variant = FBF_VARIANT_FUSED;  // spatial.hpp:102-104: box windows and sigma < 2 stay direct
+  }
   if (variant == FBF_VARIANT_FUSED && !fused_supported(f->radius, f->kind == FBF_SPATIAL_BOX)) variant = FBF_VARIANT_NAIVE;
   P.L = layout_of(gp, f->radius, variant);
   if (!workspace || workspace_bytes < P.L.total)
@@ -647,6 +660,15 @@ int fbf_filter_prepared_device(const fbf_geometry* gp, const fbf_filter* f, floa
 int fbf_bilateral_fast_device(const fbf_geometry* gp, const fbf_filter* f, const float* src,
                               float* dst, void* workspace, size_t workspace_bytes,
                               unsigned long long* d_bad, int variant, void* stream) {
+  if (variant == FBF_VARIANT_RECURSIVE) {
+    int rc = check_geometry(gp);
+    if (rc) return rc;
+    if ((rc = check_filter(f))) return rc;
+    if (uses_iir(f))
+      return iir_bilateral<float, float>(gp, f, src, dst, workspace, workspace_bytes, d_bad,
+                                         static_cast<cudaStream_t>(stream));
+    variant = FBF_VARIANT_FUSED;
+  }
   int rc = fbf_prepare_device(gp, f, src, workspace, workspace_bytes, variant, stream);
   if (rc) return rc;
   return fbf_filter_prepared_device(gp, f, dst, workspace, workspace_bytes, d_bad, variant, stream);
@@ -716,6 +738,10 @@ int fbf_finish_device(const fbf_geometry* gp, const fbf_filter* f, const float* 
 
 int fbf_launches_per_call(const fbf_geometry* g, const fbf_filter* f, int variant) {
   if (!f || !g) return 0;
+  if (variant == FBF_VARIANT_RECURSIVE) {
+    if (uses_iir(f)) return g->batch * (6 * (f->N + 1) + 1);  // per harmonic: modulate, 2 IIR, 2 transposes, demod
+    variant = FBF_VARIANT_FUSED;
+  }
   if (variant == FBF_VARIANT_FUSED && fused_supported(f->radius, f->kind == FBF_SPATIAL_BOX)) {
     const int chunks = (f->N + kMaxD) / kMaxD;  // fused launches of <= kMaxD harmonics
     if (chunks > 1) return 1 + chunks;
@@ -791,6 +817,59 @@ std::vector<Chunk> plan_chunks(const fbf_geometry* g, int W, int variant) {
 
 }  // namespace
 
+}  // extern "C"
+
+namespace {
+// Host-buffer entry of the recursive backend: whole images, fp64 inside,
+// T-typed host buffers in and out (the f64 entry keeps the reference's doubles).
+template <class T>
+int iir_host(const fbf_geometry* g, const fbf_filter* f, const T* src, T* dst, long long* bad_index) {
+  fbf_geometry gd = *g;
+  gd.src_pitch = g->width;
+  gd.dst_pitch = g->width;
+  gd.src_bstride = static_cast<long long>(g->src_rows) * g->width;
+  gd.dst_bstride = static_cast<long long>(g->out_rows) * g->width;
+  const size_t src_bytes = static_cast<size_t>(gd.src_bstride) * g->batch * sizeof(T);
+  const size_t dst_bytes = static_cast<size_t>(gd.dst_bstride) * g->batch * sizeof(T);
+  const size_t ws_bytes = iir_workspace_bytes(g, f->radius);
+  HostCtx* ctx = nullptr;
+  int rc = host_ctx(align256(src_bytes) + align256(dst_bytes) + ws_bytes + 256, ctx);
+  if (rc) return rc;
+  cudaStream_t st = ctx->st;
+  T* d_src = reinterpret_cast<T*>(ctx->buf);
+  T* d_dst = reinterpret_cast<T*>(ctx->buf + align256(src_bytes));
+  char* ws = ctx->buf + align256(src_bytes) + align256(dst_bytes);
+  unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(ws + ws_bytes);
+  for (int b = 0; b < g->batch; ++b)
+    FBF_CUDA(cudaMemcpy2DAsync(d_src + b * gd.src_bstride, g->width * sizeof(T), src + b * g->src_bstride,
+                               g->src_pitch * sizeof(T), g->width * sizeof(T), g->src_rows,
+                               cudaMemcpyHostToDevice, st));
+  FBF_CUDA(cudaMemsetAsync(d_bad, 0xFF, sizeof(unsigned long long), st));
+  rc = iir_bilateral<T, T>(&gd, f, d_src, d_dst, ws, ws_bytes, d_bad, st);
+  if (rc) {
+    cudaStreamSynchronize(st);
+    return rc;
+  }
+  for (int b = 0; b < g->batch; ++b)
+    FBF_CUDA(cudaMemcpy2DAsync(dst + b * g->dst_bstride, g->dst_pitch * sizeof(T), d_dst + b * gd.dst_bstride,
+                               g->width * sizeof(T), g->width * sizeof(T), g->out_rows, cudaMemcpyDeviceToHost,
+                               st));
+  unsigned long long bad = ~0ULL;
+  FBF_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
+  FBF_CUDA(cudaStreamSynchronize(st));
+  if (bad != ~0ULL) {
+    if (bad_index) *bad_index = static_cast<long long>(bad);
+    const long long per = static_cast<long long>(g->width) * g->height;
+    const long long inimg = static_cast<long long>(bad) % per;
+    return fail(FBF_EANOMALY, "bilateral_fast: numerical anomaly, denominator collapsed at pixel (" +
+                                  std::to_string(inimg % g->width) + ", " + std::to_string(inimg / g->width) + ")");
+  }
+  return FBF_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const float* src,
                             float* dst, int variant, long long* bad_index) {
   int rc = check_geometry(g);
@@ -798,6 +877,10 @@ int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const fl
   if ((rc = check_filter(f))) return rc;
   if ((rc = check_halo(g, f->radius))) return rc;
   int v = variant;
+  if (v == FBF_VARIANT_RECURSIVE) {
+    if (uses_iir(f)) return iir_host<float>(g, f, src, dst, bad_index);
+    v = FBF_VARIANT_FUSED;  // box windows and sigma < 2 stay direct (spatial.hpp:102-104)
+  }
   if (v == FBF_VARIANT_FUSED && !fused_supported(f->radius, f->kind == FBF_SPATIAL_BOX)) v = FBF_VARIANT_NAIVE;
   const std::vector<Chunk> chunks = plan_chunks(g, f->radius, v);
   const int K = static_cast<int>(chunks.size());
@@ -930,6 +1013,7 @@ int fbf_bilateral_fast_host_f64(const fbf_geometry* g, const fbf_filter* f, cons
   if (rc) return rc;
   if ((rc = check_filter(f))) return rc;  // validate before touching the device
   if ((rc = check_halo(g, f->radius))) return rc;
+  if (variant == FBF_VARIANT_RECURSIVE && uses_iir(f)) return iir_host<double>(g, f, src, dst, bad_index);
   fbf_geometry gd = *g;
   gd.src_pitch = g->width;
   gd.dst_pitch = g->width;

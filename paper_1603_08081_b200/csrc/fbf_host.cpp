@@ -96,23 +96,22 @@ namespace {
 }
 
 // The reference's recursive backend substitutes an IIR Gaussian only for a
-// Gaussian window with sigma >= 2 (spatial.hpp:103-105); that approximate
-// backend is outside this build, everything else is the direct path.
-void require_direct(const SpatialKernel& k, ConvolutionBackend backend, const char* who) {
-    if (backend == ConvolutionBackend::recursive && k.kind == SpatialKind::gaussian &&
-        k.sigma_s >= 2.0)
-        throw std::invalid_argument(std::string(who) +
-                                    ": the recursive (IIR) backend is not part of the B200 build");
+// Gaussian window with sigma >= 2 (spatial.hpp:103-105); everything else is
+// the direct path.  Both run on the GPU (the IIR in fp64, csrc/fbf_iir.cu).
+bool uses_iir(const SpatialKernel& k, ConvolutionBackend backend) {
+    return backend == ConvolutionBackend::recursive && k.kind == SpatialKind::gaussian && k.sigma_s >= 2.0;
 }
 
 }  // namespace
 
 Plane convolve(const Plane& plane, const SpatialKernel& kernel, ConvolutionBackend backend) {
     if (plane.width <= 0 || plane.height <= 0) throw std::invalid_argument("convolve: empty plane");
-    require_direct(kernel, backend, "convolve");
     Plane out(plane.width, plane.height);
-    const int rc = fbf_convolve_host_f64(plane.width, plane.height, kernel.profile.data(),
-                                         kernel.radius, plane.values.data(), out.values.data());
+    const int rc = uses_iir(kernel, backend)
+                       ? fbf_convolve_recursive_host_f64(plane.width, plane.height, kernel.sigma_s,
+                                                         plane.values.data(), out.values.data())
+                       : fbf_convolve_host_f64(plane.width, plane.height, kernel.profile.data(), kernel.radius,
+                                               plane.values.data(), out.values.data());
     if (rc != FBF_OK) rethrow_status(rc);
     return out;
 }
@@ -436,7 +435,6 @@ Image bilateral_fast(const Image& image, const SpatialKernel& spatial,
         throw std::invalid_argument(
             "bilateral_fast: kernel approximation error must stay below the center "
             "spatial weight");
-    require_direct(spatial, backend, "bilateral_fast");
     fbf_geometry g;
     fbf_geometry_whole(&g, image.width, image.height, 1);
     fbf_filter f{};
@@ -449,11 +447,13 @@ Image bilateral_fast(const Image& image, const SpatialKernel& spatial,
     f.omega = approx.omega;
     f.max_pointwise_error = approx.max_pointwise_error;
     f.check_epsilon = 1;
+    f.sigma_s = spatial.sigma_s;
     Image out(image.width, image.height);
     long long bad = -1;
-    const int rc =
-        fbf_bilateral_fast_host_f64(&g, &f, image.values.data(), out.values.data(),
-                                    FBF_VARIANT_FUSED, &bad);
+    const int rc = fbf_bilateral_fast_host_f64(&g, &f, image.values.data(), out.values.data(),
+                                               uses_iir(spatial, backend) ? FBF_VARIANT_RECURSIVE
+                                                                          : FBF_VARIANT_FUSED,
+                                               &bad);
     if (rc != FBF_OK) rethrow_status(rc);
     return out;
 }

@@ -97,9 +97,21 @@ def test_deterministic_box_and_recursive(tmp_path):
     assert cli(*args)[0] == 0
     assert (open(out, "rb").read(), open(rep).read()) == first
     assert cli("--input", src, "--output", out, "--sigma-s", 1.7, "--sigma-r", 30, "--spatial", "box")[0] == 0
-    # the IIR backend is not part of the B200 build: a clear error, not a silent fallback
+    # the recursive (IIR) backend, as the reference test suite runs it (test_cli.cpp BoxSpatialAndRecursiveBackend)
     rc, _, err = cli("--input", src, "--output", out, "--sigma-s", 2, "--sigma-r", 30, "--backend", "recursive")
-    assert rc == 1 and "error:" in err and "recursive" in err
+    assert rc == 0, err
+
+
+def test_recursive_backend_matches_reference_run(tmp_path, ref):
+    rng = np.random.default_rng(44)
+    src, ours, theirs = (str(tmp_path / n) for n in ("r.pgm", "r_o.pgm", "r_t.pgm"))
+    write_pgm(src, np.clip(rng.normal(120, 50, (36, 44)), 0, 255))
+    rc, _, err = cli("--input", src, "--output", ours, "--sigma-s", 2.5, "--sigma-r", 25, "--backend", "recursive")
+    assert rc == 0, err
+    # the reference driver with the recursive backend: build the same run through its run()
+    rc_t, _, err_t = ref.cli_run(src, theirs, 2.5, 25.0, 1e-3, backend=1)
+    assert rc_t == 0, err_t
+    assert np.array_equal(read_pgm(ours), read_pgm(theirs))
 
 
 def test_tabulated_ones_is_a_plain_blur(tmp_path, oracle):
