@@ -74,6 +74,7 @@ __global__ void iir_columns(const double* __restrict__ in, double* __restrict__ 
   double* __restrict__ t = tmp + static_cast<long long>(blockIdx.y) * m * cols + x;
   double* __restrict__ dst = out + plane + x;
   double y1 = src[static_cast<long long>(mirror_index(-c.pad, rows)) * cols], y2 = y1, y3 = y1;
+#pragma unroll 8
   for (int i = 0; i < m; ++i) {  // forward; start-up state = the first padded sample
     const double y = vyv_step(c, src[static_cast<long long>(mirror_index(i - c.pad, rows)) * cols], y1, y2, y3);
     t[static_cast<long long>(i) * cols] = y;
@@ -82,6 +83,7 @@ __global__ void iir_columns(const double* __restrict__ in, double* __restrict__ 
     y1 = y;
   }
   y1 = y2 = y3 = t[static_cast<long long>(m - 1) * cols];
+#pragma unroll 8
   for (int i = m - 1; i >= 0; --i) {  // backward
     const double y = vyv_step(c, t[static_cast<long long>(i) * cols], y1, y2, y3);
     if (i >= c.pad && i < c.pad + rows) dst[static_cast<long long>(i - c.pad) * cols] = y;
@@ -107,32 +109,49 @@ __global__ void transpose_planes(const double* __restrict__ in, double* __restri
   }
 }
 
-// bilateral.hpp:126-133: planes 0..3 = f cos, f sin, cos, sin of phase = (omega n) f
+// bilateral.hpp:126-133 for harmonics n0 .. n0+hb-1: planes [h][0..3] =
+// f cos, f sin, cos, sin of phase = (omega n) f
 template <class T>
-__global__ void modulate_f64(const T* __restrict__ src, int pitch, int rows, int cols, double freq,
+__global__ void modulate_f64(const T* __restrict__ src, int pitch, int rows, int cols, double omega, int n0, int hb,
                              double* __restrict__ planes) {
   const long long px = static_cast<long long>(rows) * cols;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < px;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int y = static_cast<int>(i / cols), x = static_cast<int>(i - static_cast<long long>(y) * cols);
     const double f = static_cast<double>(src[static_cast<long long>(y) * pitch + x]);
-    double s, c;
-    sincos(__dmul_rn(freq, f), &s, &c);
-    planes[i] = __dmul_rn(c, f);
-    planes[px + i] = __dmul_rn(s, f);
-    planes[2 * px + i] = c;
-    planes[3 * px + i] = s;
+    for (int h = 0; h < hb; ++h) {
+      double s, c;
+      sincos(__dmul_rn(omega * (n0 + h), f), &s, &c);  // freq = omega * n (bilateral.hpp:127)
+      double* p = planes + 4 * h * px;
+      p[i] = __dmul_rn(c, f);
+      p[px + i] = __dmul_rn(s, f);
+      p[2 * px + i] = c;
+      p[3 * px + i] = s;
+    }
   }
 }
 
-// bilateral.hpp:138-144: P += d_n (cos fcos_s + sin fsin_s), Q += d_n (cos cos_s + sin sin_s)
-__global__ void demod_f64(const double* __restrict__ mod, const double* __restrict__ conv, long long px, double dn,
-                          double* __restrict__ P, double* __restrict__ Q) {
+constexpr int kIirBlock = 16;  // harmonics per modulate / IIR / demod round
+struct DnBlock {
+  double d[kIirBlock];
+};
+
+// bilateral.hpp:138-144, harmonics in ascending order:
+// P += d_n (cos fcos_s + sin fsin_s), Q += d_n (cos cos_s + sin sin_s)
+__global__ void demod_f64(const double* __restrict__ mod, const double* __restrict__ conv, long long px, int hb,
+                          DnBlock dn, double* __restrict__ P, double* __restrict__ Q) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < px;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const double c = mod[2 * px + i], s = mod[3 * px + i];
-    P[i] = __dadd_rn(P[i], __dmul_rn(dn, __dadd_rn(__dmul_rn(c, conv[i]), __dmul_rn(s, conv[px + i]))));
-    Q[i] = __dadd_rn(Q[i], __dmul_rn(dn, __dadd_rn(__dmul_rn(c, conv[2 * px + i]), __dmul_rn(s, conv[3 * px + i]))));
+    double p = P[i], q = Q[i];
+    for (int h = 0; h < hb; ++h) {
+      const double* m = mod + 4 * h * px;
+      const double* v = conv + 4 * h * px;
+      const double c = m[2 * px + i], s = m[3 * px + i];
+      p = __dadd_rn(p, __dmul_rn(dn.d[h], __dadd_rn(__dmul_rn(c, v[i]), __dmul_rn(s, v[px + i]))));
+      q = __dadd_rn(q, __dmul_rn(dn.d[h], __dadd_rn(__dmul_rn(c, v[2 * px + i]), __dmul_rn(s, v[3 * px + i]))));
+    }
+    P[i] = p;
+    Q[i] = q;
   }
 }
 
@@ -168,14 +187,22 @@ struct IirLayout {
   size_t a, b, c, tmp, p, q, total;
 };
 
+// harmonics per round: as many as fit ~4 GB of planes (more independent
+// recursions per launch: one thread per column and plane), at most kIirBlock
+int iir_block(int width, int height, int pad) {
+  const double per = 8.0 * 4 * (3.0 * width * height + double(std::max(width, height) + 2 * pad) * std::max(width, height));
+  return std::max(1, std::min(kIirBlock, static_cast<int>(4.0e9 / per)));
+}
+
 IirLayout iir_layout(int width, int height, int pad) {
   const size_t px = static_cast<size_t>(width) * height;
-  const size_t tmp = 4 * static_cast<size_t>(std::max(width, height) + 2 * pad) * std::max(width, height);
+  const size_t hb = static_cast<size_t>(iir_block(width, height, pad));
+  const size_t tmp = 4 * hb * static_cast<size_t>(std::max(width, height) + 2 * pad) * std::max(width, height);
   IirLayout L{};
   L.a = 0;
-  L.b = L.a + align256(4 * px * 8);
-  L.c = L.b + align256(4 * px * 8);
-  L.tmp = L.c + align256(4 * px * 8);
+  L.b = L.a + align256(4 * hb * px * 8);
+  L.c = L.b + align256(4 * hb * px * 8);
+  L.tmp = L.c + align256(4 * hb * px * 8);
   L.p = L.tmp + align256(tmp * 8);
   L.q = L.p + align256(px * 8);
   L.total = L.q + align256(px * 8);
@@ -185,9 +212,11 @@ IirLayout iir_layout(int width, int height, int pad) {
 }  // namespace
 
 // workspace of the recursive path for spatial radius W (sigma <= W / 3)
+// the workspace is sized from the radius: W = ceil(3 sigma) bounds the pad
+int iir_pad_bound(int radius) { return static_cast<int>(std::ceil(4.0 * radius / 3.0)) + 13; }
+
 size_t iir_workspace_bytes(const fbf_geometry* g, int radius) {
-  const int pad = static_cast<int>(std::ceil(4.0 * radius / 3.0)) + 13;
-  return iir_layout(g->width, g->height, pad).total;
+  return iir_layout(g->width, g->height, iir_pad_bound(radius)).total;
 }
 
 // bilateral_fast with the recursive backend: whole images (the recursion runs
@@ -199,7 +228,10 @@ int iir_bilateral(const fbf_geometry* g, const fbf_filter* f, const Tin* src, To
   if (g->src_row0 != 0 || g->src_rows != g->height || g->out_row0 != 0 || g->out_rows != g->height)
     return fail(FBF_EUNSUPPORTED, "bilateral_fast: the recursive backend filters whole images only");
   const Vyv c = vyv_coeffs(f->sigma_s);
-  const IirLayout L = iir_layout(g->width, g->height, c.pad);
+  const int pad_bound = iir_pad_bound(f->radius);
+  if (c.pad > pad_bound)
+    return fail(FBF_EINVAL, "bilateral_fast: sigma_s does not match the window radius (W = ceil(3 sigma))");
+  const IirLayout L = iir_layout(g->width, g->height, pad_bound);
   if (!ws || ws_bytes < L.total) return fail(FBF_EINVAL, "bilateral_fast: workspace too small (recursive backend)");
   char* base = static_cast<char*>(ws);
   double* A = reinterpret_cast<double*>(base + L.a);
@@ -211,15 +243,19 @@ int iir_bilateral(const fbf_geometry* g, const fbf_filter* f, const Tin* src, To
   const int rows = g->height, cols = g->width;
   const long long px = static_cast<long long>(rows) * cols;
   const double q_floor = (f->w0 - f->max_pointwise_error) / 2.0;
+  const int HB = iir_block(g->width, g->height, pad_bound);
   for (int b = 0; b < g->batch; ++b) {
     FBF_CUDA(cudaMemsetAsync(P, 0, px * 8, st));
     FBF_CUDA(cudaMemsetAsync(Q, 0, px * 8, st));
-    for (int n = 0; n <= f->N; ++n) {
+    for (int n0 = 0; n0 <= f->N; n0 += HB) {
+      const int hb = std::min(HB, f->N + 1 - n0);
       modulate_f64<Tin><<<grid_1d(px), 256, 0, st>>>(src + b * g->src_bstride, static_cast<int>(g->src_pitch), rows,
-                                                     cols, f->omega * n, A);
-      FBF_CUDA(cudaMemcpyAsync(C, A, 4 * px * 8, cudaMemcpyDeviceToDevice, st));
-      FBF_CUDA(iir_planes(C, B, T, rows, cols, 4, c, st));
-      demod_f64<<<grid_1d(px), 256, 0, st>>>(A, C, px, f->d[n], P, Q);
+                                                     cols, f->omega, n0, hb, A);
+      FBF_CUDA(cudaMemcpyAsync(C, A, 4 * hb * px * 8, cudaMemcpyDeviceToDevice, st));
+      FBF_CUDA(iir_planes(C, B, T, rows, cols, 4 * hb, c, st));
+      DnBlock dn{};
+      for (int h = 0; h < hb; ++h) dn.d[h] = f->d[n0 + h];
+      demod_f64<<<grid_1d(px), 256, 0, st>>>(A, C, px, hb, dn, P, Q);
     }
     divide_f64<Tout><<<grid_1d(px), 256, 0, st>>>(P, Q, rows, cols, static_cast<int>(g->dst_pitch), q_floor,
                                                    static_cast<unsigned long long>(b) * px, d_bad,
