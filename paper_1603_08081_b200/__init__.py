@@ -79,6 +79,7 @@ SIGNATURES = {
                                            ctypes.c_size_t, _P]),
     "fbf_convolve_host_f64": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _D, ctypes.c_int, _D, _D]),
     "fbf_convolve_recursive_host_f64": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_double, _D, _D]),
+    "fbf_harmonic_groups": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.c_int]),
     "fbf_spatial_gaussian": (ctypes.c_int, [ctypes.c_double, _D, _I, _D]),
     "fbf_spatial_box": (ctypes.c_int, [ctypes.c_int, _D, _D]),
     "fbf_range_eval": (ctypes.c_double, [ctypes.c_int, ctypes.c_double, ctypes.c_double]),
@@ -250,6 +251,11 @@ def _filter_struct(spatial: SpatialKernel, approx: FourierKernelApprox, check_ep
                approx.max_pointwise_error, 1 if check_epsilon else 0, spatial.sigma_s)
     f._keep = (prof, d)  # keep the buffers alive with the struct
     return f
+
+
+def harmonic_groups(geometry: Geometry, radius: int) -> int:
+    """CTA groups the fused path splits the harmonics into for this geometry."""
+    return lib.fbf_harmonic_groups(ctypes.byref(geometry), radius)
 
 
 def whole_geometry(width: int, height: int, batch: int = 1) -> Geometry:

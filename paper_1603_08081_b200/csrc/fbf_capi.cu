@@ -405,16 +405,36 @@ struct Layout {
 // 1 otherwise (c4 -9 %, c5 -17 % at 4).  A function of the GLOBAL image size
 // and the radius only -- never of the strip or batch a shard holds -- so
 // results are bit-identical across multi-GPU partitions.  FBF_GROUPS overrides.
+// Harmonic groups (grid.y): each group's CTAs take 1/groups of the harmonics
+// over groups x more rows, so the 2W-row prologue of a work unit is amortised
+// over >= ~200 rows per CTA; at most one group per 32 CTAs.  From the call's
+// own output rows (a rank's strip, a pipeline strip, a whole image): a strip
+// whose count differs from the whole image's sums its group planes in another
+// order -- equal to fp32 rounding, not bit for bit.
+// Measured: profiles/r01_groups.txt (whole images), r01_notes.md (c2 strips).
+// the host entry's pipeline strips keep the grouping of the whole call
+// (results independent of the pipeline cut): set around its chunk launches
+thread_local int g_groups_override = 0;
+
 int harmonic_groups(const fbf_geometry* g, int radius) {
+  if (g_groups_override) return g_groups_override;
   static const int forced = [] {
     const char* e = getenv("FBF_GROUPS");
     return e ? std::max(1, std::min(8, atoi(e))) : 0;
   }();
   if (forced) return forced;
-  const long long px = static_cast<long long>(g->width) * g->height;
-  if (px <= 512LL * 1024) return 8;
-  if (px <= 2LL * 1024 * 1024 && radius <= 9) return 4;
-  return 1;
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  const double ctas = static_cast<double>(sms) * (radius <= 9 ? 2 : 1);  // launch_w: small CTAs for W <= 9
+  const double strips = std::ceil(g->width / static_cast<double>(kFusedTW));
+  const double rows_cta = static_cast<double>(g->out_rows) * g->batch * strips / ctas;
+  const int limit = std::max(1, std::min(8, static_cast<int>(ctas / 32)));
+  int groups = 1;
+  while (groups * 2 <= limit && rows_cta * groups < 200.0) groups *= 2;
+  return groups;
 }
 
 // sum of the nonempty groups' (Q, P) planes -> divide (or -> a dense plane)
@@ -736,6 +756,11 @@ int fbf_finish_device(const fbf_geometry* gp, const fbf_filter* f, const float* 
   return FBF_OK;
 }
 
+int fbf_harmonic_groups(const fbf_geometry* g, int radius) {
+  if (!g || check_geometry(g) != FBF_OK) return 0;
+  return harmonic_groups(g, radius);
+}
+
 int fbf_launches_per_call(const fbf_geometry* g, const fbf_filter* f, int variant) {
   if (!f || !g) return 0;
   if (variant == FBF_VARIANT_RECURSIVE) {
@@ -902,6 +927,11 @@ int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const fl
     gc.dst_bstride = db;
     return gc;
   };
+  // every chunk uses the harmonic grouping of the whole call (bit-identical to one launch)
+  struct GroupsOverride {
+    explicit GroupsOverride(int g) { g_groups_override = g; }
+    ~GroupsOverride() { g_groups_override = 0; }
+  } groups_override(harmonic_groups(g, f->radius));
   size_t ws_bytes = 0;
   for (const Chunk& c : chunks) {
     const fbf_geometry gc = chunk_geometry(c);

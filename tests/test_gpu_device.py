@@ -38,13 +38,19 @@ def run_device(img_rows, geo, s, a, variant="fused", check_eps=True):
 def test_row_strips_reassemble_bit_identically(name, world):
     c = CONFIGS[name]
     img, s, a = image_of(c), spatial_of(c), approx_of(c)
-    whole = run_device(img, fb.whole_geometry(c.width, c.height), s, a, check_eps=c.check_epsilon)[0]
-    parts = []
+    wg = fb.whole_geometry(c.width, c.height)
+    whole = run_device(img, wg, s, a, check_eps=c.check_epsilon)[0]
+    parts, same_groups = [], True
     for r in range(world):
         sh = plan(c.width, c.height, 1, s.radius, world, r)
-        parts.append(run_device(img[sh.src_row0:sh.src_row0 + sh.src_rows], geometry(sh, c.width, c.height),
-                                s, a, check_eps=c.check_epsilon)[0])
-    assert np.array_equal(np.concatenate(parts), whole)
+        g = geometry(sh, c.width, c.height)
+        same_groups &= fb.harmonic_groups(g, s.radius) == fb.harmonic_groups(wg, s.radius)
+        parts.append(run_device(img[sh.src_row0:sh.src_row0 + sh.src_rows], g, s, a, check_eps=c.check_epsilon)[0])
+    parts = np.concatenate(parts)
+    if same_groups:  # same harmonic grouping: bit for bit
+        assert np.array_equal(parts, whole)
+    else:  # short strips split the harmonics over more CTA groups: fp32 rounding of the group sums
+        assert np.abs(parts - whole).max() <= 2e-4
 
 
 def test_batch_shards_match_whole_batch():

@@ -59,9 +59,14 @@ def test_c5_batch_images(oracle):
     for k, i in enumerate(idx):
         ref = oracle_rows(oracle, batch[k], s, a, True, 500, 532)
         assert maxabs(gpu[k, 500:532], ref) <= TOL
-        # batched result == the image filtered alone, bit for bit
+        # batched result == the image filtered alone: bit for bit with the same
+        # harmonic grouping, else to fp32 rounding of the group sums
         alone = fb.bilateral_fast(batch[k], s, a)
-        assert np.array_equal(alone, gpu[k])
+        if fb.harmonic_groups(fb.whole_geometry(c.width, c.height, 3), s.radius) == \
+                fb.harmonic_groups(fb.whole_geometry(c.width, c.height), s.radius):
+            assert np.array_equal(alone, gpu[k])
+        else:
+            assert maxabs(alone, gpu[k]) <= 2e-4
 
 
 @pytest.mark.parametrize("name", list(CONFIGS))
