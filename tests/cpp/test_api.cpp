@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <random>
 #include <sstream>
 #include <stdexcept>
@@ -117,6 +118,34 @@ static void host_checks() {
       [&] { bilateral_fast(random_integer_image(8, 8, 7), make_spatial_gaussian(3.0), bad); }));
   CHECK(throws<std::invalid_argument>([] { local_dynamic_range(Image(), 1); }));
   CHECK(throws<std::invalid_argument>([] { local_dynamic_range(Image(4, 4, 0.0), 0); }));
+}
+
+// test_pgm.cpp / test_cli.cpp restated (host-only parts: the codec, run()'s diagnostics)
+static void pgm_cli_host_checks() {
+  const Image one = decode_pgm(std::string("P5\n1 1\n255\n") + static_cast<char>(0x80));
+  CHECK(one.width == 1 && one.height == 1 && one(0, 0) == 128.0);
+  const Image c = decode_pgm(std::string("P5 # c\n# line\n  2 1 # dims\n255\n") + static_cast<char>(3) +
+                             static_cast<char>(250));
+  CHECK(c.width == 2 && c(0, 0) == 3.0 && c(1, 0) == 250.0);
+  CHECK(decode_pgm("P2\n2 1\n255\n7 9\n")(1, 0) == 9.0);
+  CHECK(throws<std::runtime_error>([] { decode_pgm("P6\n1 1\n255\nx"); }, "not a P5 or P2"));
+  CHECK(throws<std::runtime_error>([] { decode_pgm("P5\n2 2\n255\nab"); }, "truncated raster"));
+  CHECK(throws<std::runtime_error>([] { decode_pgm("P2\n1 1\n100\n101"); }, "exceeds maxval"));
+  Image r(5, 1);
+  r.values = {0.5, 1.49, 254.5, -3.0, 300.0};
+  const Image back = decode_pgm(encode_pgm(r));
+  CHECK(back.values == (std::vector<double>{1.0, 1.0, 255.0, 0.0, 255.0}));
+  CHECK(throws<std::invalid_argument>([] { encode_pgm(Image()); }));
+  CHECK(throws<std::runtime_error>([] { read_pgm("/nonexistent/file.pgm"); }));
+  CliOptions opt;  // run(): diagnostics before any pixel work
+  std::ostringstream out, err;
+  CHECK(run(opt, out, err) == 1 && err.str().find("--input") != std::string::npos);
+  opt.input_path = "/nonexistent/in.pgm";
+  opt.output_path = "/tmp/unused.pgm";
+  opt.sigma_s = 1.0;
+  opt.sigma_r = 30.0;
+  err.str("");
+  CHECK(run(opt, out, err) == 1 && err.str().find("error:") != std::string::npos);
 }
 
 static void gpu_checks() {
@@ -239,11 +268,43 @@ static void gpu_checks() {
       }
     CHECK(throws<std::invalid_argument>([&] { convolve(Plane(), k); }));
   }
+  // the recursive backend (spatial.hpp:98-112 dispatch, recursive_gaussian.hpp)
+  {
+    const Image img = random_integer_image(24, 20, 31);
+    const SpatialKernel narrow = make_spatial_gaussian(1.5), wide = make_spatial_gaussian(3.0);
+    CHECK(convolve(img, narrow, ConvolutionBackend::recursive).values == convolve(img, narrow).values);
+    const Plane iir = convolve(img, wide, ConvolutionBackend::recursive), fir = convolve(img, wide);
+    CHECK(linf_error(iir, fir) > 1e-6 && linf_error(iir, fir) < 5.0);
+    const FourierKernelApprox a = progressive_fit(RangeKernel::gaussian(30.0), 255, 1e-3);
+    const Image bi = bilateral_fast(img, make_spatial_gaussian(2.5), a, ConvolutionBackend::recursive);
+    CHECK(linf_error(bi, bilateral_fast(img, make_spatial_gaussian(2.5), a)) < 5.0);
+  }
+  // cli.hpp run() end to end: PGM in, report out
+  {
+    const std::string in = "/tmp/fbf_test_api_in.pgm", outp = "/tmp/fbf_test_api_out.pgm",
+                      rep = "/tmp/fbf_test_api_report.txt";
+    write_pgm(random_integer_image(20, 14, 5), in);
+    CliOptions opt;
+    opt.input_path = in;
+    opt.output_path = outp;
+    opt.report_path = rep;
+    opt.sigma_s = 1.0;
+    opt.sigma_r = 30.0;
+    opt.compare_exact = true;
+    std::ostringstream o, e;
+    CHECK(run(opt, o, e) == 0);
+    CHECK(read_pgm(outp).width == 20);
+    std::ifstream f(rep);
+    std::stringstream txt;
+    txt << f.rdbuf();
+    CHECK(txt.str().find("measured_linf=") != std::string::npos);
+  }
 }
 
 int main(int argc, char** argv) {
   const bool host_only = argc > 1 && std::strcmp(argv[1], "--host") == 0;
   host_checks();
+  pgm_cli_host_checks();
   if (!host_only) gpu_checks();
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;
