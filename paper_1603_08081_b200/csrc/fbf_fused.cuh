@@ -63,7 +63,15 @@ struct FusedCfg {
   static constexpr size_t OFF_STAGE = 0;
   static constexpr size_t OFF_PQ = up128(OFF_STAGE + size_t(G) * MW * 8);
   static constexpr size_t OFF_M = up128(OFF_PQ + size_t(G) * TW * 8);  // planes A, B
-  static constexpr size_t OFF_R = OFF_M + 2 * size_t(G) * MP * 8;      // planes A, B
+  static constexpr size_t M_BYTES = 2 * size_t(G) * MP * 8;
+  static constexpr size_t bytes_with(int nmb) {
+    return up128(OFF_M + nmb * M_BYTES + 2 * size_t(RING) * RP * 8 + size_t(CRING) * CP * 8) + 16;
+  }
+  // M double-buffered where it fits: the next step's modulation then writes the
+  // other buffer, and the row pass -> column pass hand-off only syncs the two
+  // warps of a column chunk (their rows and columns) instead of the whole CTA
+  static constexpr int NMB = NT > 128 && bytes_with(2) <= 227 * 1024 ? 2 : 1;  // small CTAs: keep 2 per SM
+  static constexpr size_t OFF_R = OFF_M + NMB * M_BYTES;  // planes A, B
   static constexpr size_t OFF_CS = OFF_R + 2 * size_t(RING) * RP * 8;
   static constexpr size_t OFF_BAR = up128(OFF_CS + size_t(CRING) * CP * 8);
   static constexpr size_t smem_bytes = OFF_BAR + 16;
@@ -287,8 +295,10 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
                                          const ModNext<C>& next, PhaseClock& clk) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int h = lane >> 4;
-  const int x = (lane & 15) + C::HALF * (warp % (C::TW / C::HALF));
-  const int gi = (warp / (C::TW / C::HALF)) * C::KC;  // first output row of this lane, rel. to o
+  // warp -> (column chunk, run) as in the row pass's (chunk, row group): the
+  // warps that row-passed a chunk's columns are the ones that read them here
+  const int x = (lane & 15) + C::HALF * (warp / (C::G / C::HALF));
+  const int gi = (warp % (C::G / C::HALF)) * C::KC;  // first output row of this lane, rel. to o
   const int r0 = o + gi;
   const int gx = u.x0 + x;
   const int nr = min(C::KC, u.y1 - r0);  // <= 0: this lane only helps with the modulation
@@ -410,7 +420,9 @@ template <class C>
 __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(const __grid_constant__ FusedArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   int2* stage = reinterpret_cast<int2*>(smem + C::OFF_STAGE);
-  p2* M = reinterpret_cast<p2*>(smem + C::OFF_M);
+  p2* M0 = reinterpret_cast<p2*>(smem + C::OFF_M);
+  unsigned mk = 0;  // step counter: this step's modulated rows are in M buffer mk & 1
+  auto m_buf = [&](unsigned k) { return M0 + (C::NMB == 2 ? (k & 1u) : 0u) * (C::M_BYTES / 8); };
   p2* R = reinterpret_cast<p2*>(smem + C::OFF_R);
   float* CS = reinterpret_cast<float*>(smem + C::OFF_CS);
   p2* pqs = reinterpret_cast<p2*>(smem + C::OFF_PQ);
@@ -469,7 +481,7 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
       }
       mbar_wait(bar_uf, ph_uf);
       ph_uf ^= 1u;
-      modulate_rows<C>(stage, M, rows, static_cast<uint32_t>(nb));
+      modulate_rows<C>(stage, m_buf(mk), rows, static_cast<uint32_t>(nb));
     }
     for (int n = nb; n < ne; ++n) {
       const bool first = n == n_first;
@@ -494,26 +506,39 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
             tma_load_3d(pqs, &A.tm_pq, bar_uf, u.x0, o - A.g.out_row0,
                         static_cast<int>(blockIdx.y) * A.g.batch + u.b);
         }
-        row_pass<C>(A, M, R, CS, a, rows, base);
+        row_pass<C>(A, m_buf(mk), R, CS, a, rows, base);
         clk.mark(2);
         if (more || want_pq) {
           mbar_wait(bar_uf, ph_uf);
           ph_uf ^= 1u;
         }
         clk.mark(3);
-        __syncthreads();  // S2: ring rows visible, next (u, f') and this step's (Q, P) landed, M free
+        // S2: this chunk's ring rows visible (the (u, f') and (Q, P) copies are
+        // covered by each thread's own barrier wait above); with one M buffer
+        // the whole CTA must also be past the row pass before M is rewritten
+        if constexpr (C::NMB == 2) {
+          if constexpr (C::G / C::HALF == 1)
+            __syncwarp();
+          else
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + static_cast<int>(threadIdx.x >> 5) / (C::G / C::HALF)),
+                         "n"(32 * (C::G / C::HALF))
+                         : "memory");
+        } else {
+          __syncthreads();
+        }
         clk.mark(4);
         // the next step's modulation is interleaved into this step's column pass
         // (its ALU work issues in the FFMA2 shadow); prologue steps run it alone
-        const ModNext<C> next{stage, M, static_cast<uint32_t>(wrap ? n + 1 : n)};
+        const ModNext<C> next{stage, m_buf(mk + 1), static_cast<uint32_t>(wrap ? n + 1 : n)};
         if (o >= 0) {
           col_pass<C>(A, R, CS, pqs, u, o, base, n - A.h.d_base, first, divide, next, clk);
           clk.mark(7);
         } else {
-          modulate_rows<C>(stage, M, rows2, next.n);
+          modulate_rows<C>(stage, next.M, rows2, next.n);
           clk.mark(6);
         }
         clk.step();
+        ++mk;
       }
     }
     pos += len;
