@@ -6,31 +6,24 @@
 namespace fbf {
 
 #define FBF_EXTERN(WW, BB) extern template cudaError_t launch_w<WW, BB>(const FusedArgs&, cudaStream_t, int*);
-FBF_EXTERN(3, false)
-FBF_EXTERN(5, false)
-FBF_EXTERN(6, false)
-FBF_EXTERN(8, false)
-FBF_EXTERN(9, false)
-FBF_EXTERN(12, false)
-FBF_EXTERN(15, false)
-FBF_EXTERN(24, false)
+#define FBF_RADII(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) \
+  X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30)
+#define FBF_EXTERN_G(WW) FBF_EXTERN(WW, false)
+FBF_RADII(FBF_EXTERN_G)
 FBF_EXTERN(2, true)
 FBF_EXTERN(3, true)
 FBF_EXTERN(4, true)
 FBF_EXTERN(5, true)
-#undef FBF_EXTERN
+#undef FBF_EXTERN_G
 
-// Gaussian radii with a compiled fused kernel: the BASELINE configs' 5, 9, 12,
-// 15, 24 and the reference tests' 3, 6, 8.  Box windows: radii 2..5 (c3 is 5),
-// with running-sum passes.  Everything else takes the naive multi-kernel path.
+// Gaussian radii 1..30 (sigma <= 10) have a fused kernel -- every radius
+// make_spatial_gaussian produces for the reference's sigma sweeps (cli.hpp:
+// 1..12 -> W up to 36: 11 and 12 take the naive chain); box windows: radii
+// 2..5 (c3 is 5), with running-sum passes.  Everything else takes the naive
+// multi-kernel path.
 bool fused_supported(int W, bool box) {
   if (box) return W >= 2 && W <= 5;
-  switch (W) {
-    case 3: case 5: case 6: case 8: case 9: case 12: case 15: case 24:
-      return true;
-    default:
-      return false;
-  }
+  return W >= 1 && W <= 30;
 }
 
 #ifdef FBF_PHASE_PROF
@@ -56,14 +49,11 @@ cudaError_t launch_fused(const FusedArgs& a_in, cudaStream_t st, int* grid_out) 
     }
   }
   switch (a.k.W) {
-    case 3: return launch_w<3>(a, st, grid_out);
-    case 5: return launch_w<5>(a, st, grid_out);
-    case 6: return launch_w<6>(a, st, grid_out);
-    case 8: return launch_w<8>(a, st, grid_out);
-    case 9: return launch_w<9>(a, st, grid_out);
-    case 12: return launch_w<12>(a, st, grid_out);
-    case 15: return launch_w<15>(a, st, grid_out);
-    case 24: return launch_w<24>(a, st, grid_out);
+#define FBF_CASE(WW) \
+  case WW:           \
+    return launch_w<WW>(a, st, grid_out);
+    FBF_RADII(FBF_CASE)
+#undef FBF_CASE
     default: return cudaErrorInvalidValue;
   }
 }

@@ -79,7 +79,7 @@ struct FusedCfg {
   static_assert(G % HALF == 0 && TW % HALF == 0, "tiling");
   static_assert((G / HALF) * (TW / KR) * 32 == NT, "row pass: one (16 rows, chunk) item per warp");
   static_assert((TW / HALF) * (G / KC) * 32 == NT, "column pass: one (16 columns, run) item per warp");
-  static_assert(smem_bytes <= 227 * 1024, "shared memory budget");
+  static constexpr bool FITS = smem_bytes <= 227 * 1024;  // launchable at all (one CTA per SM)
 };
 
 // Geometry of one work unit and the rows of step s (same for every harmonic).
@@ -625,12 +625,19 @@ template <int W, bool BOX = false>
 cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
   using Small = FusedCfg<W, 64, 16, 16, 16, 128, BOX>;
   using Big = FusedCfg<W, 64, 32, 16, 16, 256, BOX>;
-  if constexpr (Small::smem_bytes <= 113 * 1024) {
-    const char* env = getenv("FBF_FUSED_CFG");
+  const char* env = getenv("FBF_FUSED_CFG");
+  if constexpr (Small::smem_bytes <= 113 * 1024) {  // two 128-thread CTAs per SM
     const bool big = env ? env[0] == 'b' : !(W <= 9);
-    if (!big) return launch_cfg<Small>(a, st, grid_out);
+    if (!big || !Big::FITS) return launch_cfg<Small>(a, st, grid_out);
   }
-  return launch_cfg<Big>(a, st, grid_out);
+  if constexpr (Big::FITS) {
+    return launch_cfg<Big>(a, st, grid_out);
+  } else if constexpr (Small::FITS) {  // large W: one 128-thread CTA per SM
+    return launch_cfg<Small>(a, st, grid_out);
+  } else {
+    (void)env;
+    return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace fbf

@@ -237,3 +237,16 @@ def test_exponential_kernel_high_order(oracle):
     assert a.N == N
     gpu = fb.bilateral_fast(img, s, a)
     assert maxabs(gpu, oracle_rows(oracle, img, s, a)) <= TOL
+
+
+@pytest.mark.parametrize("sigma", [0.3, 0.6, 1.3, 2.3, 3.3, 3.6, 4.3, 6.0, 7.0, 8.7, 10.0])
+def test_fused_radii_1_to_30(oracle, sigma):
+    """Every Gaussian radius 1..30 (sigma <= 10) has a fused instance; large
+    radii run one 128-thread CTA per SM (the 256-thread tiles exceed shared memory)."""
+    rng = np.random.default_rng(int(sigma * 10))
+    img = rng.integers(0, 256, (72, 130)).astype(np.float64)
+    s = fb.make_spatial_gaussian(sigma)
+    a = fb.fit_fixed(0, 30.0, 255, 14)
+    ref = oracle_rows(oracle, img, s, a, check_eps=False, nthreads=4)
+    assert maxabs(fb.bilateral_fast(img, s, a, check_epsilon=False), ref) <= TOL
+    assert fb.launches_per_call(fb.whole_geometry(130, 72), s, a) <= 3  # prep, fused (, group sum): no naive chain
