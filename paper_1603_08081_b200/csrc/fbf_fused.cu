@@ -10,19 +10,19 @@ namespace fbf {
   X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30)
 #define FBF_EXTERN_G(WW) FBF_EXTERN(WW, false)
 FBF_RADII(FBF_EXTERN_G)
-FBF_EXTERN(2, true)
-FBF_EXTERN(3, true)
-FBF_EXTERN(4, true)
-FBF_EXTERN(5, true)
+#define FBF_BOX_RADII(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
+#define FBF_EXTERN_B(WW) FBF_EXTERN(WW, true)
+FBF_BOX_RADII(FBF_EXTERN_B)
 #undef FBF_EXTERN_G
+#undef FBF_EXTERN_B
 
-// Gaussian radii 1..30 (sigma <= 10) have a fused kernel -- every radius
-// make_spatial_gaussian produces for the reference's sigma sweeps (cli.hpp:
-// 1..12 -> W up to 36: 11 and 12 take the naive chain); box windows: radii
-// 2..5 (c3 is 5), with running-sum passes.  Everything else takes the naive
-// multi-kernel path.
+// Gaussian radii 1..30 (sigma <= 10) have a fused kernel -- make_spatial_gaussian
+// gives W = ceil(3 sigma), so the reference CLI's sweep (cli.hpp: sigma 1..12)
+// leaves only sigma 11 and 12 to the naive chain; box windows: radii 1..16
+// (c3 is 5; the CLI's box radius is ceil(sigma)), with running-sum passes.
+// Everything else takes the naive multi-kernel path.
 bool fused_supported(int W, bool box) {
-  if (box) return W >= 2 && W <= 5;
+  if (box) return W >= 1 && W <= 16;
   return W >= 1 && W <= 30;
 }
 
@@ -41,10 +41,11 @@ cudaError_t launch_fused(const FusedArgs& a_in, cudaStream_t st, int* grid_out) 
 #endif
   if (a.k.box) {
     switch (a.k.W) {
-      case 2: return launch_w<2, true>(a, st, grid_out);
-      case 3: return launch_w<3, true>(a, st, grid_out);
-      case 4: return launch_w<4, true>(a, st, grid_out);
-      case 5: return launch_w<5, true>(a, st, grid_out);
+#define FBF_CASE_B(WW) \
+  case WW:             \
+    return launch_w<WW, true>(a, st, grid_out);
+      FBF_BOX_RADII(FBF_CASE_B)
+#undef FBF_CASE_B
       default: return cudaErrorInvalidValue;
     }
   }

@@ -103,9 +103,9 @@ def test_edge_shapes_all_radii(oracle, shape, sigma):
     assert maxabs(fb.bilateral_fast(img, s, a), oracle_rows(oracle, img, s, a, nthreads=1)) <= TOL
 
 
-@pytest.mark.parametrize("radius", [1, 2, 4, 7])
-def test_box_and_radii_without_fused_instance(oracle, radius):
-    """Radii with no fused instantiation take the naive chain; box windows."""
+@pytest.mark.parametrize("radius", [1, 2, 4, 7, 10, 16, 17])
+def test_box_radii(oracle, radius):
+    """Box windows: running-sum fused instances for radii 1..16, the naive chain beyond."""
     rng = np.random.default_rng(radius)
     img = rng.integers(0, 256, (37, 45)).astype(np.float64)
     s = fb.make_spatial_box(radius)
