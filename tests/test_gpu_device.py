@@ -92,3 +92,34 @@ def test_pipelined_host_path_reports_the_first_collapse():
     lying = fb.FourierKernelApprox(255, np.pi / 255, 0, np.array([0.0]), 0.0, 0.0)
     with pytest.raises(fb.FilterError, match=r"pixel \(0, 0\)"):
         fb.bilateral_fast(img, fb.make_spatial_gaussian(2.0), lying)
+
+
+def test_host_entry_is_reentrant_across_threads():
+    """bilateral.hpp's contract (SURVEY §8(b) threading): pure and reentrant;
+    the host entry keeps one stream / buffer / graph per calling thread."""
+    import threading
+    c = CONFIGS["c1"]
+    s, a = spatial_of(c), approx_of(c)
+    rng = np.random.default_rng(77)
+    imgs = [np.clip(rng.normal(128, 60, (300 + 40 * k, 280)), 0, 255).astype(np.float32) for k in range(4)]
+    want = [fb.bilateral_fast(im, s, a) for im in imgs]
+    got = [[None] * 4 for _ in range(2)]
+    errors = []
+
+    def worker(t):
+        try:
+            for rep in range(3):
+                for k in range(4):
+                    got[t][k] = fb.bilateral_fast(imgs[(k + t) % 4], s, a)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(2)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors
+    for t in range(2):
+        for k in range(4):
+            assert np.array_equal(got[t][k], want[(k + t) % 4])
