@@ -75,7 +75,10 @@ struct FusedCfg {
   static constexpr size_t OFF_CS = OFF_R + 2 * size_t(RING) * RP * 8;
   static constexpr size_t OFF_BAR = up128(OFF_CS + size_t(CRING) * CP * 8);
   static constexpr size_t smem_bytes = OFF_BAR + 16;
-  static_assert(KR == 16 && KC == 16, "one lane per (half, 16 outputs)");
+  static_assert(KR == KC && (KR == 16 || KR == 8), "one lane per (half, KR outputs)");
+  // warps sharing one 16-column chunk: the row-pass producers and column-pass
+  // consumers of that chunk's ring columns (the S2 hand-off group)
+  static constexpr int CHUNK_WARPS = (NT / 32) / (TW / HALF);
   static_assert(G % HALF == 0 && TW % HALF == 0, "tiling");
   static_assert((G / HALF) * (TW / KR) * 32 == NT, "row pass: one (16 rows, chunk) item per warp");
   static_assert((TW / HALF) * (G / KC) * 32 == NT, "column pass: one (16 columns, run) item per warp");
@@ -297,8 +300,8 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
   const int h = lane >> 4;
   // warp -> (column chunk, run) as in the row pass's (chunk, row group): the
   // warps that row-passed a chunk's columns are the ones that read them here
-  const int x = (lane & 15) + C::HALF * (warp / (C::G / C::HALF));
-  const int gi = (warp % (C::G / C::HALF)) * C::KC;  // first output row of this lane, rel. to o
+  const int x = (lane & 15) + C::HALF * (warp / (C::G / C::KC));
+  const int gi = (warp % (C::G / C::KC)) * C::KC;  // first output row of this lane, rel. to o
   const int r0 = o + gi;
   const int gx = u.x0 + x;
   const int nr = min(C::KC, u.y1 - r0);  // <= 0: this lane only helps with the modulation
@@ -517,11 +520,11 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
         // covered by each thread's own barrier wait above); with one M buffer
         // the whole CTA must also be past the row pass before M is rewritten
         if constexpr (C::NMB == 2) {
-          if constexpr (C::G / C::HALF == 1)
+          if constexpr (C::CHUNK_WARPS == 1)
             __syncwarp();
           else
-            asm volatile("bar.sync %0, %1;" ::"r"(1 + static_cast<int>(threadIdx.x >> 5) / (C::G / C::HALF)),
-                         "n"(32 * (C::G / C::HALF))
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + static_cast<int>(threadIdx.x >> 5) / C::CHUNK_WARPS),
+                         "n"(32 * C::CHUNK_WARPS)
                          : "memory");
         } else {
           __syncthreads();
@@ -625,7 +628,11 @@ template <int W, bool BOX = false>
 cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
   using Small = FusedCfg<W, 64, 16, 16, 16, 128, BOX>;
   using Big = FusedCfg<W, 64, 32, 16, 16, 256, BOX>;
+  using Wide = FusedCfg<W, 64, 32, 8, 8, 512, BOX>;  // Big's tile, 8 outputs per lane, 4 warps per SMSP
   const char* env = getenv("FBF_FUSED_CFG");
+  if constexpr (!BOX && Wide::FITS) {
+    if (env && env[0] == 'w') return launch_cfg<Wide>(a, st, grid_out);
+  }
   if constexpr (Small::smem_bytes <= 113 * 1024) {  // two 128-thread CTAs per SM
     const bool big = env ? env[0] == 'b' : !(W <= 9);
     if (!big || !Big::FITS) return launch_cfg<Small>(a, st, grid_out);
