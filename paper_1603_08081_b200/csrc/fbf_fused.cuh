@@ -628,11 +628,7 @@ template <int W, bool BOX = false>
 cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
   using Small = FusedCfg<W, 64, 16, 16, 16, 128, BOX>;
   using Big = FusedCfg<W, 64, 32, 16, 16, 256, BOX>;
-  using Wide = FusedCfg<W, 64, 32, 8, 8, 512, BOX>;  // Big's tile, 8 outputs per lane, 4 warps per SMSP
   const char* env = getenv("FBF_FUSED_CFG");
-  if constexpr (!BOX && Wide::FITS) {
-    if (env && env[0] == 'w') return launch_cfg<Wide>(a, st, grid_out);
-  }
   if constexpr (Small::smem_bytes <= 113 * 1024) {  // two 128-thread CTAs per SM
     const bool big = env ? env[0] == 'b' : !(W <= 9);
     if (!big || !Big::FITS) return launch_cfg<Small>(a, st, grid_out);
