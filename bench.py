@@ -7,9 +7,11 @@ One step = one pass of the hot path (phase prep + fused filter kernel) over the
 workload's synthetic input, inputs resident in HBM.  Default workload: BASELINE
 config c2 (2048x2048 fp32, Gaussian sigma_s=5 / W=15, Gaussian sigma_r=20,
 N=20), the config BASELINE.json's metric is quoted on that fits one GPU.  With
-N GPUs (torchrun, one process per GPU) the image is split into N row strips,
-each carrying W halo rows (no collective on the data path; the total work is
-fixed -> strong scaling); batch configs (c5) split by image.
+N GPUs (torchrun, one process per GPU) and the default `--scaling weak`, every
+rank filters its own copy of the workload (the same shapes, its own seeds:
+seed + 1000 * rank), so the work per GPU is fixed and there is no collective
+on the data path.  `--scaling strong` instead splits the one workload: a single
+image into N row strips, each carrying W halo rows, a batch (c5) by image.
 
 Printed on rank 0: ONE JSON line (metric/value/unit/.../roofline/cpu_baseline/
 e2e/gpu_launches/clocks).  `--impl reference` times the reference's own CPU
@@ -42,6 +44,8 @@ def parse():
     p.add_argument("--config", default="c2")
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--variant", default="fused", choices=["fused", "naive"])
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="N>1: weak = one whole workload per rank (own seeds), strong = split one workload")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--profile-once", action="store_true",
@@ -157,9 +161,9 @@ def run_reference(args, cfg, world, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE.json generator, include/fourierbf_b200.h fbf_synth_image)",
-        "config": config_dict(cfg, world),
+        "config": config_dict(cfg, world, args.scaling),
         "cpu_baseline": {"value": value, "unit": "Mpixel/s", "cores": nthreads, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -168,11 +172,13 @@ def run_reference(args, cfg, world, rank):
     return 0
 
 
-def config_dict(cfg, world):
+def config_dict(cfg, world, scaling="weak"):
     return {"workload": cfg.name, "width": cfg.width, "height": cfg.height, "batch": cfg.batch,
             "spatial": cfg.spatial, "sigma_s": cfg.sigma_s, "W": cfg.radius,
             "range": "exponential" if cfg.range_family else "gaussian", "sigma_r": cfg.sigma_r, "N": cfg.N,
-            "T": 255, "parallelism": (f"row-strips-x{world}" if cfg.batch == 1 else f"images-x{world}"),
+            "T": 255,
+            "parallelism": (f"workload-per-rank-x{world}" if scaling == "weak" or world == 1 else
+                            f"row-strips-x{world}" if cfg.batch == 1 else f"images-x{world}"),
             "l2": "flushed between steps (512 MiB write)"}
 
 
@@ -202,12 +208,17 @@ def main():
 
     spatial, approx = spatial_of(cfg), approx_of(cfg)
     W = spatial.radius
-    part = plan(cfg.width, cfg.height, cfg.batch, W, world, rank)
+    weak = args.scaling == "weak"
+    # weak: this rank's own whole workload; strong: its share of the one workload
+    part = plan(cfg.width, cfg.height, cfg.batch, W, 1 if weak else world, 0 if weak else rank)
     geo = shard_geometry(part, cfg.width, cfg.height)
+    seed_off = 1000 * rank if weak else 0
     if cfg.batch > 1:
-        host = np.stack([image_of(cfg, i) for i in part.images])
-    else:  # each rank generates only its own strip (with halo rows)
-        host = image_of(cfg, 0, part.src_row0, part.src_rows)[None]
+        host = np.stack([fb.synth_image(cfg.seeds[i] + seed_off, cfg.width, cfg.height, cfg.rects, cfg.noise)
+                         for i in part.images])
+    else:  # each rank generates only its own rows (with halo rows)
+        host = fb.synth_image(cfg.seeds[0] + seed_off, cfg.width, cfg.height, cfg.rects, cfg.noise,
+                              part.src_row0, part.src_rows)[None]
     nb = host.shape[0]
     src = torch.from_numpy(host).to(dev)
     dst = torch.empty((nb, geo.out_rows, cfg.width), dtype=torch.float32, device=dev)
@@ -320,10 +331,10 @@ def main():
             }
         line = {
             "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (BASELINE.json generator, seeded; include/fourierbf_b200.h fbf_synth_image)",
-            "config": config_dict(cfg, world),
+            "config": config_dict(cfg, world, args.scaling),
             "variant": args.variant,
             "roofline": roof,
             "gpu_launches": args.steps * fb.launches_per_call(geo, spatial, approx, args.variant),
