@@ -459,8 +459,20 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
     const long long r = p - sidx * A.g.out_rows;
     return sidx * A.g.out_rows + (r - r % C::KC);
   };
-  const long long lo = blockIdx.x == 0 ? 0 : split(total * blockIdx.x / gridDim.x);
-  const long long hi = blockIdx.x + 1 == gridDim.x ? total : split(total * (blockIdx.x + 1) / gridDim.x);
+  // Cost-balanced cuts: every work unit (strip of an image) also pays its
+  // prologue, ~unit_cost rows, so a CTA whose range crosses a strip boundary
+  // gets that many fewer rows.  Cuts are equally spaced in the cost coordinate
+  // c(p) = p + unit_cost * (units before p); its inverse maps a target back to
+  // a row position (a target inside a boundary's jump lands on the boundary).
+  const long long per = static_cast<long long>(A.g.out_rows) + A.unit_cost;
+  const long long ctotal = total / A.g.out_rows * per;
+  auto cut = [&](long long k) {
+    const long long t = ctotal * k / gridDim.x;
+    const long long s = t / per;
+    return split(s * A.g.out_rows + min(t - s * per, static_cast<long long>(A.g.out_rows)));
+  };
+  const long long lo = blockIdx.x == 0 ? 0 : cut(blockIdx.x);
+  const long long hi = blockIdx.x + 1 == gridDim.x ? total : cut(blockIdx.x + 1);
   for (long long pos = lo; pos < hi;) {
     const long long sidx = pos / A.g.out_rows;
     const int r0 = static_cast<int>(pos - sidx * A.g.out_rows);
@@ -581,6 +593,15 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
   a.strips = (a.g.width + C::TW - 1) / C::TW;
   a.pq_cols = a.strips * C::TW;
   a.total = static_cast<long long>(a.g.batch) * a.strips * a.g.out_rows;
+  // a unit's prologue row-passes 2W rows without a column pass or demodulation
+  // (~55 % of a full row's cost, measured: FBF_UNIT_COST_PCT sweep)
+  {
+    static const int pct = [] {
+      const char* e = getenv("FBF_UNIT_COST_PCT");
+      return e ? atoi(e) : 55;
+    }();
+    a.unit_cost = 2 * W * pct / 100;
+  }
   cudaError_t e = encode_tile_3d(&a.tm_uf, a.uf, static_cast<unsigned long long>(a.pq_cols + 2 * W),
                                  static_cast<unsigned long long>(a.g.out_rows + 2 * W),
                                  static_cast<unsigned long long>(a.g.batch), C::MW, C::G);

@@ -73,6 +73,7 @@ struct FusedArgs {
   int strips;              // ceil(width / TW)
   long long total;         // batch * strips * out_rows
   int seg_max;             // longest row run one CTA filters in one pass over n
+  int unit_cost;           // extra cost of one work unit (its 2W-row prologue + bootstrap) in output rows
   unsigned long long* prof;  // phase cycle counters (FBF_PHASE_PROF builds only), else null
   int accumulate;  // 1: the launch's first harmonic adds to the (Q, P) planes instead of initialising them
   Harmonics h;     // last: the coefficient block is the large member
