@@ -99,10 +99,10 @@ int fbf_filter_prepared_device(const fbf_geometry* g, const fbf_filter* f, float
                                void* workspace, size_t workspace_bytes,
                                unsigned long long* d_bad, int variant, void* stream);
 /* Harmonic groups (CTA groups splitting the harmonics, each with its own
- * (Q, P) plane) the fused path uses for this geometry and radius.  Calls on
- * different geometries (e.g. row strips of one image) with different group
- * counts agree to fp32 rounding of the group sums, not bit for bit. */
-int fbf_harmonic_groups(const fbf_geometry* g, int radius);
+ * (Q, P) plane) the fused path uses for this geometry, radius and order N.
+ * Calls on different geometries (e.g. row strips of one image) with different
+ * group counts agree to fp32 rounding of the group sums, not bit for bit. */
+int fbf_harmonic_groups(const fbf_geometry* g, int radius, int N);
 /* Kernel launches one fbf_bilateral_fast_device call makes. */
 int fbf_launches_per_call(const fbf_geometry* g, const fbf_filter* f, int variant);
 

@@ -79,7 +79,7 @@ SIGNATURES = {
                                            ctypes.c_size_t, _P]),
     "fbf_convolve_host_f64": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _D, ctypes.c_int, _D, _D]),
     "fbf_convolve_recursive_host_f64": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_double, _D, _D]),
-    "fbf_harmonic_groups": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.c_int]),
+    "fbf_harmonic_groups": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.c_int, ctypes.c_int]),
     "fbf_spatial_gaussian": (ctypes.c_int, [ctypes.c_double, _D, _I, _D]),
     "fbf_spatial_box": (ctypes.c_int, [ctypes.c_int, _D, _D]),
     "fbf_range_eval": (ctypes.c_double, [ctypes.c_int, ctypes.c_double, ctypes.c_double]),
@@ -253,9 +253,9 @@ def _filter_struct(spatial: SpatialKernel, approx: FourierKernelApprox, check_ep
     return f
 
 
-def harmonic_groups(geometry: Geometry, radius: int) -> int:
-    """CTA groups the fused path splits the harmonics into for this geometry."""
-    return lib.fbf_harmonic_groups(ctypes.byref(geometry), radius)
+def harmonic_groups(geometry: Geometry, radius: int, N: int) -> int:
+    """CTA groups the fused path splits the N+1 harmonics into for this geometry."""
+    return lib.fbf_harmonic_groups(ctypes.byref(geometry), radius, N)
 
 
 def whole_geometry(width: int, height: int, batch: int = 1) -> Geometry:

@@ -408,44 +408,66 @@ struct Layout {
 
 // Harmonic split inside one GPU: the harmonics are divided among CTA groups,
 // each accumulating its own (Q, P) plane, summed in a fixed order at the end.
-// Each group's CTAs get work units with `groups` times more rows, which cuts
-// the per-unit 2W-row prologue by that factor and keeps small images from
-// degenerating into very short units; large images lose to the extra (Q, P)
-// traffic.  Measured (profiles/r01_groups.txt): 8 groups for <= 0.5 Mpx
-// images (c1 1575 -> 3142 Mpx/s), 4 for <= 2 Mpx with W <= 9 (c3 3124 -> 3939),
-// 1 otherwise (c4 -9 %, c5 -17 % at 4).  A function of the GLOBAL image size
-// and the radius only -- never of the strip or batch a shard holds -- so
-// results are bit-identical across multi-GPU partitions.  FBF_GROUPS overrides.
-// Harmonic groups (grid.y): each group's CTAs take 1/groups of the harmonics
-// over groups x more rows, so the 2W-row prologue of a work unit is amortised
-// over >= ~200 rows per CTA; at most one group per 32 CTAs.  From the call's
-// own output rows (a rank's strip, a pipeline strip, a whole image): a strip
-// whose count differs from the whole image's sums its group planes in another
-// order -- equal to fp32 rounding, not bit for bit.
-// Measured: profiles/r01_groups.txt (whole images), r01_notes.md (c2 strips).
+// Each group's CTAs get work units with `groups` times more rows and 1/groups
+// of the harmonics, which cuts the per-harmonic 2W-row unit prologues; large
+// images lose to the extra (Q, P) planes and the finish pass.  The count comes
+// from a cost model (group_model) of the call's own output rows (a rank's
+// strip, a pipeline strip, a whole image) and harmonic count: a strip whose
+// count differs from the whole image's sums its group planes in another order
+// -- equal to fp32 rounding, not bit for bit.
+// Measured: profiles/r01_groups.txt, r01_notes.md.  FBF_GROUPS overrides.
 // the host entry's pipeline strips keep the grouping of the whole call
 // (results independent of the pipeline cut): set around its chunk launches
 thread_local int g_groups_override = 0;
 
-int harmonic_groups(const fbf_geometry* g, int radius) {
-  if (g_groups_override) return g_groups_override;
+int forced_groups() {
   static const int forced = [] {
     const char* e = getenv("FBF_GROUPS");
     return e ? std::max(1, std::min(8, atoi(e))) : 0;
   }();
-  if (forced) return forced;
+  return forced;
+}
+
+// Cost model, in CTA rows of one harmonic: a CTA of group count k filters
+// ceil(H / k) harmonics over R / floor(ctas / k) rows, each harmonic paying
+// its unit's prologue (~0.55 * 2W rows, the fused kernel's unit cost).  A
+// larger k must win by 3 %: the extra (Q, P) planes and the finish pass are
+// not in the model (measured: c1 13 harmonics -> 7 groups, c3 31 -> 4,
+// c2 21 -> 1; profiles/r01_notes.md).
+int group_model(const fbf_geometry* g, int radius, int H) {
   static const int sms = [] {
     int dev = 0, n = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n > 0 ? n : 148;
   }();
-  const double ctas = static_cast<double>(sms) * (radius <= 9 ? 2 : 1);  // launch_w: small CTAs for W <= 9
+  const int ctas = sms * (radius <= 9 ? 2 : 1);  // launch_w: small CTAs for W <= 9
   const double strips = std::ceil(g->width / static_cast<double>(kFusedTW));
-  const double rows_cta = static_cast<double>(g->out_rows) * g->batch * strips / ctas;
-  const int limit = std::max(1, std::min(8, static_cast<int>(ctas / 32)));
+  const double rows = static_cast<double>(g->out_rows) * g->batch * strips;
+  const double u = 2.0 * radius * 0.55;
+  auto cost = [&](int k) { return ((H + k - 1) / k) * (rows / (ctas / k) + u); };
   int groups = 1;
-  while (groups * 2 <= limit && rows_cta * groups < 200.0) groups *= 2;
+  double best = cost(1);
+  for (int k = 2; k <= std::min({8, H, ctas}); ++k) {
+    const double c = cost(k);
+    if (c < 0.97 * best) best = c, groups = k;
+  }
   return groups;
+}
+
+// (Q, P) planes the workspace holds for this geometry: the most any harmonic
+// count (per launch: <= kMaxD) picks
+int group_cap(const fbf_geometry* g, int radius) {
+  if (g_groups_override) return g_groups_override;
+  if (forced_groups()) return forced_groups();
+  int cap = 1;
+  for (int H = 2; H <= kMaxD && cap < 8; ++H) cap = std::max(cap, group_model(g, radius, H));
+  return cap;
+}
+
+int harmonic_groups(const fbf_geometry* g, int radius, int harmonics) {
+  if (g_groups_override) return g_groups_override;
+  if (forced_groups()) return forced_groups();
+  return std::min(group_model(g, radius, std::min(harmonics, kMaxD)), group_cap(g, radius));
 }
 
 // sum of the nonempty groups' (Q, P) planes -> divide (or -> a dense plane)
@@ -491,7 +513,7 @@ Layout layout_of(const fbf_geometry* g, int radius, int variant) {
     const size_t cols = static_cast<size_t>((g->width + kFusedTW - 1) / kFusedTW) * kFusedTW;
     const size_t uf_px = static_cast<size_t>(g->batch) * (g->out_rows + 2 * radius) * (cols + 2 * radius);
     L.pq = align256(uf_px * sizeof(int2));
-    L.total = L.pq + align256(static_cast<size_t>(harmonic_groups(g, radius)) * g->batch * g->out_rows * cols *
+    L.total = L.pq + align256(static_cast<size_t>(group_cap(g, radius)) * g->batch * g->out_rows * cols *
                               sizeof(Pair));
     return L;
   }
@@ -654,7 +676,7 @@ int fbf_filter_prepared_device(const fbf_geometry* gp, const fbf_filter* f, floa
     A.bad = d_bad;
     A.seg_max = 1 << 30;
     cudaError_t e = cudaSuccess;
-    const int groups = launch_fused_range(A, f, 0, P.H.N + 1, harmonic_groups(gp, f->radius), false, st, &e);
+    const int groups = launch_fused_range(A, f, 0, P.H.N + 1, harmonic_groups(gp, f->radius, P.H.N + 1), false, st, &e);
     FBF_CUDA(e);
     if (groups > 1) {
       const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
@@ -724,7 +746,7 @@ int fbf_partial_sums_device(const fbf_geometry* gp, const fbf_filter* f, int n_l
     A.pq = P.pq;
     A.seg_max = 1 << 30;
     cudaError_t e = cudaSuccess;
-    const int groups = launch_fused_range(A, f, n_lo, n_hi, harmonic_groups(gp, f->radius), true, st, &e);
+    const int groups = launch_fused_range(A, f, n_lo, n_hi, harmonic_groups(gp, f->radius, n_hi - n_lo), true, st, &e);
     FBF_CUDA(e);
     const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
     const long long plane = static_cast<long long>(P.G.batch) * P.G.out_rows * cols;
@@ -767,9 +789,9 @@ int fbf_finish_device(const fbf_geometry* gp, const fbf_filter* f, const float* 
   return FBF_OK;
 }
 
-int fbf_harmonic_groups(const fbf_geometry* g, int radius) {
-  if (!g || check_geometry(g) != FBF_OK) return 0;
-  return harmonic_groups(g, radius);
+int fbf_harmonic_groups(const fbf_geometry* g, int radius, int N) {
+  if (!g || check_geometry(g) != FBF_OK || N < 0) return 0;
+  return std::min(harmonic_groups(g, radius, N + 1), N + 1);
 }
 
 int fbf_launches_per_call(const fbf_geometry* g, const fbf_filter* f, int variant) {
@@ -781,7 +803,7 @@ int fbf_launches_per_call(const fbf_geometry* g, const fbf_filter* f, int varian
   if (variant == FBF_VARIANT_FUSED && fused_supported(f->radius, f->kind == FBF_SPATIAL_BOX)) {
     const int chunks = (f->N + kMaxD) / kMaxD;  // fused launches of <= kMaxD harmonics
     if (chunks > 1) return 1 + chunks;
-    return std::min(harmonic_groups(g, f->radius), f->N + 1) > 1 ? 3 : 2;  // prep, fused (, group sum)
+    return std::min(harmonic_groups(g, f->radius, f->N + 1), f->N + 1) > 1 ? 3 : 2;  // prep, fused (, group sum)
   }
   return 1 + 4 * (f->N + 1) + 1;
 }
@@ -942,7 +964,7 @@ int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const fl
   struct GroupsOverride {
     explicit GroupsOverride(int g) { g_groups_override = g; }
     ~GroupsOverride() { g_groups_override = 0; }
-  } groups_override(harmonic_groups(g, f->radius));
+  } groups_override(harmonic_groups(g, f->radius, f->N + 1));
   size_t ws_bytes = 0;
   for (const Chunk& c : chunks) {
     const fbf_geometry gc = chunk_geometry(c);

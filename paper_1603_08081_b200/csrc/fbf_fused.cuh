@@ -630,8 +630,10 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
     info.dev = dev;
   }
   const int sms = info.sms, occ = info.occ;
-  // one wave in total: the harmonic groups share the SMs
-  long long grid = (static_cast<long long>(sms) * occ + a.groups - 1) / a.groups;
+  // one wave in total: the harmonic groups share the SMs (rounded down: a
+  // group count that does not divide the resident CTAs must not spill into a
+  // second wave)
+  long long grid = static_cast<long long>(sms) * occ / a.groups;
   // keep at least ~2W+G rows per CTA so the per-unit prologue stays amortised
   const long long min_rows = 2 * C::W + C::G;
   const long long by_work = (a.total + min_rows - 1) / min_rows;

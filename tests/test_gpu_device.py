@@ -44,7 +44,7 @@ def test_row_strips_reassemble_bit_identically(name, world):
     for r in range(world):
         sh = plan(c.width, c.height, 1, s.radius, world, r)
         g = geometry(sh, c.width, c.height)
-        same_groups &= fb.harmonic_groups(g, s.radius) == fb.harmonic_groups(wg, s.radius)
+        same_groups &= fb.harmonic_groups(g, s.radius, a.N) == fb.harmonic_groups(wg, s.radius, a.N)
         parts.append(run_device(img[sh.src_row0:sh.src_row0 + sh.src_rows], g, s, a, check_eps=c.check_epsilon)[0])
     parts = np.concatenate(parts)
     if same_groups:  # same harmonic grouping: bit for bit

@@ -62,8 +62,8 @@ def test_c5_batch_images(oracle):
         # batched result == the image filtered alone: bit for bit with the same
         # harmonic grouping, else to fp32 rounding of the group sums
         alone = fb.bilateral_fast(batch[k], s, a)
-        if fb.harmonic_groups(fb.whole_geometry(c.width, c.height, 3), s.radius) == \
-                fb.harmonic_groups(fb.whole_geometry(c.width, c.height), s.radius):
+        if fb.harmonic_groups(fb.whole_geometry(c.width, c.height, 3), s.radius, a.N) == \
+                fb.harmonic_groups(fb.whole_geometry(c.width, c.height), s.radius, a.N):
             assert np.array_equal(alone, gpu[k])
         else:
             assert maxabs(alone, gpu[k]) <= 2e-4
