@@ -459,8 +459,16 @@ int group_model(const fbf_geometry* g, int radius, int H) {
 int group_cap(const fbf_geometry* g, int radius) {
   if (g_groups_override) return g_groups_override;
   if (forced_groups()) return forced_groups();
+  // a few hundred model evaluations: memoised per thread (the host entry asks
+  // several times per call)
+  struct Memo {
+    int out_rows = -1, width = -1, batch = -1, radius = -1, cap = 1;
+  };
+  thread_local Memo m;
+  if (m.out_rows == g->out_rows && m.width == g->width && m.batch == g->batch && m.radius == radius) return m.cap;
   int cap = 1;
   for (int H = 2; H <= kMaxD && cap < 8; ++H) cap = std::max(cap, group_model(g, radius, H));
+  m = Memo{g->out_rows, g->width, g->batch, radius, cap};
   return cap;
 }
 
