@@ -50,6 +50,10 @@ template <int W_, int TW_, int G_, int KR_, int KC_, int NT_, bool BOX_ = false>
 struct FusedCfg {
   static constexpr int W = W_, TW = TW_, G = G_, KR = KR_, KC = KC_, NT = NT_;
   static constexpr bool BOX = BOX_;
+  // deferred demodulation (Pending): measured gains on the 256-thread Gaussian
+  // kernels only (c2 +0.9 %, c4 +3.6 %); the short running-sum row pass of the
+  // box path cannot hide it (c3 -4.6 %) and the 128-thread kernels break even
+  static constexpr bool DEFER = !BOX_ && NT_ > 128;
   static constexpr int MW = TW + 2 * W;   // modulated row width
   static constexpr int MP = MW | 1;       // M plane pitch in 8-byte units (odd: conflict-free row walks)
   static constexpr int RING = 2 * W + G;  // R ring rows
@@ -230,18 +234,57 @@ struct PhaseClock {
 #endif
 };
 
+// Deferred demodulation.  The column pass leaves this lane's (c|s)-weighted
+// partials of its KC output rows and their running (Q, P) in registers; the
+// NEXT step's row pass finishes them (swap halves with the partner lane,
+// accumulate, store) between its FFMA2s, so the demodulation's latency chain
+// (loads -> multiply -> shuffle -> add -> store) no longer stalls both warps of
+// an SMSP at the end of every column pass.  Divide steps (last harmonic) and a
+// unit's last step finish immediately.
+template <class C>
+struct Pending {
+  static constexpr int KH = C::KC / 2;
+  p2 part[C::KC];  // c * acc (half A) or s * acc (half B), rows gi .. gi+KC-1
+  p2 pq[KH];       // running (Q, P) of this lane's output rows (0 at the first harmonic)
+  p2 dd;           // (d_n, d_n)
+  p2* dst;         // (Q, P) of this lane's first output row; rows A.pq_cols apart
+  int nh;          // rows this lane stores (<= 0: nothing pending)
+  // output row k of this lane: (q, p) = own half + partner's half
+  __device__ __forceinline__ p2 qp(int k, int h) const {
+    const p2 send = h ? part[k] : part[KH + k];
+    const p2 own = h ? part[KH + k] : part[k];
+    return add2(own, __shfl_xor_sync(0xffffffffu, send, 16));
+  }
+  // (Q, P) += d_n (q, p)
+  __device__ __forceinline__ void finish(int k, int h, int stride) const {
+    const p2 v = fma2(dd, qp(k, h), pq[k]);
+    if (k < nh) dst[k * stride] = v;
+  }
+};
+
 // Row pass: warp = (16 rows, one KR-chunk of output columns); lane l filters
 // row g of half h = l / 16 (plane A or B) into the R ring, and stores its
 // half of the centre (c, s) of each input row's KR pixels into the CS ring.
 template <class C>
 __device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restrict__ M, p2* __restrict__ R,
-                                         float* __restrict__ CS, int a, int rows, int base) {
+                                         float* __restrict__ CS, int a, int rows, int base,
+                                         const Pending<C>& pd) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int h = lane >> 4;
   const int g = (lane & 15) + C::HALF * (warp % (C::G / C::HALF));
   const int xc = (warp / (C::G / C::HALF)) * C::KR;
-  if (g >= rows) return;
+  // no early exit: rows past the step's end filter stale (finite) M rows and
+  // only their stores are predicated, so every lane stays converged for the
+  // deferred demodulation's shuffles interleaved below
+  const bool live = g < rows;
+  if (!C::DEFER && !live) return;
   const p2* __restrict__ src = M + (h * C::G + g) * C::MP + xc;
+  constexpr int TAPS_IN = C::KR + 2 * C::W;
+  auto defer_at = [&](int m) {  // finish pending row k at input position m (compile-time)
+#pragma unroll
+    for (int k = 0; k < Pending<C>::KH; ++k)
+      if (C::DEFER && m == k * TAPS_IN / Pending<C>::KH) pd.finish(k, h, A.pq_cols);
+  };
   const int rel = a + g - base;
   const int slot = rel % C::RING;
   float* __restrict__ csrow = CS + 2 * (rel % C::CRING) * C::CP + h;
@@ -253,7 +296,8 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restric
     for (int m = 0; m <= 2 * C::W; ++m) {
       const p2 v = src[m];
       sum = add2(sum, v);
-      if (m >= C::W && m < C::W + C::KR) csrow[2 * (xc + m - C::W)] = lo_of(v);
+      if (m >= C::W && m < C::W + C::KR && live) csrow[2 * (xc + m - C::W)] = lo_of(v);
+      defer_at(m);
     }
     acc[0] = sum;
 #pragma unroll
@@ -262,7 +306,8 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restric
       sum = sub2(add2(sum, vin), vout);
       acc[i] = sum;
       const int m = i + 2 * C::W;
-      if (m >= C::W && m < C::W + C::KR) csrow[2 * (xc + m - C::W)] = lo_of(vin);
+      if (m >= C::W && m < C::W + C::KR && live) csrow[2 * (xc + m - C::W)] = lo_of(vin);
+      defer_at(2 * C::W + i);
     }
   } else {
 #pragma unroll
@@ -278,13 +323,16 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restric
           acc[i] = fma2(pk(tv, tv), v, acc[i]);
         }
       }
-      if (m >= C::W && m < C::W + C::KR)  // centre of output column xc + m - W
+      if (m >= C::W && m < C::W + C::KR && live)  // centre of output column xc + m - W
         csrow[2 * (xc + m - C::W)] = lo_of(v);
+      defer_at(m);
     }
   }
-  p2* __restrict__ dst = R + (h * C::RING + slot) * C::RP + xc;
+  if (live) {
+    p2* __restrict__ dst = R + (h * C::RING + slot) * C::RP + xc;
 #pragma unroll
-  for (int i = 0; i < C::KR; ++i) dst[i] = acc[i];
+    for (int i = 0; i < C::KR; ++i) dst[i] = acc[i];
+  }
 }
 
 // Column pass: warp = (16 columns, one KC-run of output rows); lane l filters
@@ -295,7 +343,7 @@ template <class C>
 __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restrict__ R,
                                          const float* __restrict__ CS, const p2* __restrict__ pqs,
                                          const Unit& u, int o, int base, int dn_idx, bool first, bool divide,
-                                         const ModNext<C>& next, PhaseClock& clk) {
+                                         bool defer, const ModNext<C>& next, PhaseClock& clk, Pending<C>& pd) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int h = lane >> 4;
   // warp -> (column chunk, run) as in the row pass's (chunk, row group): the
@@ -306,14 +354,20 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
   const int gx = u.x0 + x;
   const int nr = min(C::KC, u.y1 - r0);  // <= 0: this lane only helps with the modulation
   p2 acc[C::KC];
+  constexpr int KH = C::KC / 2;
   const p2* __restrict__ Rh = R + h * C::RING * C::RP + x;
   const int s0 = (r0 - C::W - base) % C::RING;
   constexpr int TAPS_IN = C::KC + 2 * C::W;
   constexpr int NBATCH = ModNext<C>::NBATCH;
-  constexpr int STRIDE = TAPS_IN / NBATCH > 0 ? TAPS_IN / NBATCH : 1;
+#ifndef FBF_MOD_OFF
+#define FBF_MOD_OFF 12
+#endif
+  constexpr int OFF = (C::BOX || TAPS_IN <= FBF_MOD_OFF + NBATCH) ? 0 : FBF_MOD_OFF;
+  constexpr int STRIDE = (TAPS_IN - OFF) / NBATCH > 0 ? (TAPS_IN - OFF) / NBATCH : 1;
   // one batch of (up to) 4 modulation elements of the next step per STRIDE taps
   auto batch = [&](int m) {
-    if (m % STRIDE == 0 && m / STRIDE < NBATCH) ModNext<C>::batch(m / STRIDE, next.stage, next.M, next.n);
+    if (m >= OFF && (m - OFF) % STRIDE == 0 && (m - OFF) / STRIDE < NBATCH)
+      ModNext<C>::batch((m - OFF) / STRIDE, next.stage, next.M, next.n);
   };
   auto ring = [&](int m) {
     int s = s0 + m;
@@ -352,60 +406,53 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
     }
   }
 #pragma unroll
-  for (int b = TAPS_IN / STRIDE + (TAPS_IN % STRIDE ? 1 : 0); b < NBATCH; ++b)
+  for (int b = (TAPS_IN - OFF + STRIDE - 1) / STRIDE; b < NBATCH; ++b)
     ModNext<C>::batch(b, next.stage, next.M, next.n);
   clk.mark(5);
   // (q, p) = c (Gc, Fc) + s (Gs, Fs)   [bilateral.hpp:138-144, real form]:
-  // this lane's half of every row, then swap halves with the partner lane
-  constexpr int KH = C::KC / 2;
+  // this lane's half of every row now; the halves meet in Pending::qp
   const int cs0 = (r0 - base) % C::CRING;
-  p2 part[C::KC];
 #pragma unroll
   for (int i = 0; i < C::KC; ++i) {
     int sc = cs0 + i;
     sc = sc >= C::CRING ? sc - C::CRING : sc;
     const float w = CS[2 * (sc * C::CP + x) + h];
-    part[i] = mul2(pk(w, w), acc[i]);
+    pd.part[i] = mul2(pk(w, w), acc[i]);
   }
-  p2 qp[KH];
+  const p2* __restrict__ pqin = pqs + (gi + h * KH) * C::TW + x;
 #pragma unroll
-  for (int k = 0; k < KH; ++k) {
-    const p2 send = h ? part[k] : part[KH + k];
-    const p2 own = h ? part[KH + k] : part[k];
-    qp[k] = add2(own, __shfl_xor_sync(0xffffffffu, send, 16));
-  }
-  if (gx >= A.g.width) return;
+  for (int k = 0; k < KH; ++k) pd.pq[k] = first ? 0ull : pqin[k * C::TW];
   const int rr = r0 + h * KH;  // first output row of this lane
-  const int nh = nr - h * KH;  // rows of this lane (may be <= 0)
-  if (nh <= 0) return;
+  pd.nh = gx < A.g.width ? nr - h * KH : 0;  // rows of this lane (may be <= 0)
   // box: both passes summed unweighted; the weight (1/(2W+1))^2 = w0 joins d_n here
   // d_n (dn_idx = n - d_base: the launch's coefficient block)
   const float dn = C::BOX ? A.h.d[dn_idx] * (A.k.box_tap * A.k.box_tap) : A.h.d[dn_idx];
-  const p2 dd = pk(dn, dn);
-  const p2* __restrict__ pqin = pqs + (gi + h * KH) * C::TW + x;
+  pd.dd = pk(dn, dn);
   if (!divide) {
-    p2* __restrict__ pqrow = reinterpret_cast<p2*>(A.pq) +
-                             ((blockIdx.y * A.g.batch + u.b) * static_cast<long long>(A.g.out_rows) +
-                              (rr - A.g.out_row0)) * A.pq_cols + gx;
-    const int wstride = A.pq_cols;
-    if (first) {
+    pd.dst = reinterpret_cast<p2*>(A.pq) +
+             ((blockIdx.y * A.g.batch + u.b) * static_cast<long long>(A.g.out_rows) + (rr - A.g.out_row0)) *
+                 A.pq_cols +
+             gx;
+    if (!defer) {
 #pragma unroll
-      for (int k = 0; k < KH; ++k)
-        if (k < nh) pqrow[k * wstride] = mul2(dd, qp[k]);
-    } else {
-#pragma unroll
-      for (int k = 0; k < KH; ++k)
-        if (k < nh) pqrow[k * wstride] = fma2(dd, qp[k], pqin[k * C::TW]);
+      for (int k = 0; k < KH; ++k) pd.finish(k, h, A.pq_cols);
+      pd.nh = 0;
     }
     return;
   }
   // bilateral.hpp:147-158: divide; flag the first collapsed denominator
+  p2 qp[KH];
+#pragma unroll
+  for (int k = 0; k < KH; ++k) qp[k] = pd.qp(k, h);
+  const int nh = pd.nh;
+  pd.nh = 0;
+  if (nh <= 0) return;
   float* __restrict__ drow = A.dst + u.b * A.g.dst_bstride +
                              static_cast<long long>(rr - A.g.out_row0) * A.g.dst_pitch + gx;
 #pragma unroll
   for (int k = 0; k < KH; ++k) {
     if (k < nh) {
-      const p2 acc2 = first ? mul2(dd, qp[k]) : fma2(dd, qp[k], pqin[k * C::TW]);
+      const p2 acc2 = fma2(pd.dd, qp[k], pd.pq[k]);
       float Q, P;
       upk(acc2, Q, P);
       if (!(fabsf(Q) >= A.h.q_floor) && A.bad) {
@@ -437,6 +484,8 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
   }
   __syncthreads();
   unsigned ph_uf = 0;  // phase parity of the next completion of the copy barrier
+  Pending<C> pd;
+  pd.nh = 0;
   PhaseClock clk;
   clk.start();
 
@@ -521,7 +570,8 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
             tma_load_3d(pqs, &A.tm_pq, bar_uf, u.x0, o - A.g.out_row0,
                         static_cast<int>(blockIdx.y) * A.g.batch + u.b);
         }
-        row_pass<C>(A, m_buf(mk), R, CS, a, rows, base);
+        row_pass<C>(A, m_buf(mk), R, CS, a, rows, base, pd);
+        pd.nh = 0;
         clk.mark(2);
         if (more || want_pq) {
           mbar_wait(bar_uf, ph_uf);
@@ -546,7 +596,12 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
         // (its ALU work issues in the FFMA2 shadow); prologue steps run it alone
         const ModNext<C> next{stage, m_buf(mk + 1), static_cast<uint32_t>(wrap ? n + 1 : n)};
         if (o >= 0) {
-          col_pass<C>(A, R, CS, pqs, u, o, base, n - A.h.d_base, first, divide, next, clk);
+          // defer the demodulation into the next row pass when there is a next
+          // step in this unit and the same rows are not re-read by TMA within
+          // two steps (nsteps > 2; the generic-proxy stores keep the same
+          // distance to the next harmonic's async-proxy (Q, P) load as before)
+          const bool defer = C::DEFER && more && !divide && nsteps > 2;
+          col_pass<C>(A, R, CS, pqs, u, o, base, n - A.h.d_base, first, divide, defer, next, clk, pd);
           clk.mark(7);
         } else {
           modulate_rows<C>(stage, next.M, rows2, next.n);

@@ -15,9 +15,11 @@ __global__ void __launch_bounds__(C::NT, 1) fir(const __grid_constant__ FusedArg
   float* CS = reinterpret_cast<float*>(smem + C::OFF_CS);
   for (int i = threadIdx.x; i < 2 * C::G * C::MP; i += blockDim.x) M[i] = pk(1.0f + i * 1e-6f, 0.5f);
   __syncthreads();
+  Pending<C> pd;
+  pd.nh = 0;
   long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
-    row_pass<C>(A, M, R, CS, it * C::G, C::G, 0);
+    row_pass<C>(A, M, R, CS, it * C::G, C::G, 0, pd);
     if (SYNC) __syncthreads();
     else asm volatile("" ::: "memory");
   }
