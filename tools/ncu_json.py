@@ -34,6 +34,7 @@ out = {
 }
 out["dram_bytes_per_launch"] = out["dram_bytes_read"] + out["dram_bytes_write"]
 for k, name in (("fma_pipe_active_pct", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                ("fma_pipe_inst_pct", "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
                 ("issue_active_pct", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
                 ("registers_per_thread", "launch__registers_per_thread"),
                 ("smem_bank_conflicts", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum")):

@@ -17,6 +17,7 @@ raw = list(csv.reader(io.StringIO(ncu("--page", "raw", "--csv"))))
 h, u, v = raw[0], raw[1], raw[2]
 want = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_fma.sum",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
         "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
