@@ -208,24 +208,27 @@ __device__ __forceinline__ void modulate_rows(const int2* __restrict__ stage, p2
 // otherwise the marks compile to nothing.
 struct PhaseClock {
 #ifdef FBF_PHASE_PROF
-  unsigned long long ph[9];  // 8 phases + step count
+  // thread 0 (the TMA leader) and thread 32 (a non-leader warp) separately:
+  // out[0..9] and out[10..19]; index 9 = step count
+  unsigned long long ph[10];
   long long t;
+  __device__ __forceinline__ bool on() const { return threadIdx.x == 0 || threadIdx.x == 32; }
   __device__ __forceinline__ void start() {
-    for (int i = 0; i < 9; ++i) ph[i] = 0;
+    for (int i = 0; i < 10; ++i) ph[i] = 0;
     t = clock64();
   }
   __device__ __forceinline__ void mark(int i) {
-    if ((threadIdx.x & 127) == 0) {
+    if (on()) {
       const long long now = clock64();
       ph[i] += now - t;
       t = now;
     }
   }
   __device__ __forceinline__ void flush(unsigned long long* out) {
-    if ((threadIdx.x & 127) == 0 && out)
-      for (int i = 0; i < 9; ++i) atomicAdd(out + i, ph[i]);
+    if (on() && out)
+      for (int i = 0; i < 10; ++i) atomicAdd(out + (threadIdx.x ? 10 : 0) + i, ph[i]);
   }
-  __device__ __forceinline__ void step() { ph[8] += (threadIdx.x & 127) == 0; }
+  __device__ __forceinline__ void step() { ph[9] += on(); }
 #else
   __device__ __forceinline__ void step() {}
   __device__ __forceinline__ void start() {}
@@ -570,6 +573,7 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
             tma_load_3d(pqs, &A.tm_pq, bar_uf, u.x0, o - A.g.out_row0,
                         static_cast<int>(blockIdx.y) * A.g.batch + u.b);
         }
+        clk.mark(8);
         row_pass<C>(A, m_buf(mk), R, CS, a, rows, base, pd);
         pd.nh = 0;
         clk.mark(2);

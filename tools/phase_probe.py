@@ -17,7 +17,8 @@ import torch  # noqa: E402
 import paper_1603_08081_b200 as fb  # noqa: E402
 from paper_1603_08081_b200.configs import CONFIGS, approx_of, image_of, spatial_of  # noqa: E402
 
-NAMES = ["loop top", "S1 wait", "row pass", "TMA waits", "S2 wait", "col FIR + next mod", "prologue mod", "demod + stores"]
+NAMES = ["loop top", "S1 wait", "row pass", "TMA waits", "S2 wait", "col FIR + next mod", "prologue mod",
+         "demod + stores", "TMA issue (leader)"]
 
 
 def main(name):
@@ -34,17 +35,16 @@ def main(name):
     buf = (ctypes.c_ulonglong * 32)()
     for rep in range(3):
         fb.bilateral_fast_device(img.data_ptr(), out.data_ptr(), geo, sp, ap, ws.data_ptr(), ws_bytes,
-                                 bad.data_ptr())
+                                 bad.data_ptr(), check_epsilon=c.check_epsilon)
         torch.cuda.synchronize()
         fn(buf)
-    steps = buf[8]
-    print(f"{name}: {steps} steps (thread 0 of every CTA), cycles per step:")
-    tot = 0
-    for i in range(8):
-        v = buf[i] / max(steps, 1)
-        tot += v
-        print(f"  {NAMES[i]:<22} {v:8.0f}")
-    print(f"  {'total':<22} {tot:8.0f}")
+    print(f"{name}: cycles per step, thread 0 (TMA leader) | thread 32 (warp 1)")
+    tot = [0, 0]
+    for i in range(9):
+        v = [buf[10 * k + i] / max(buf[10 * k + 9], 1) for k in (0, 1)]
+        tot = [tot[k] + v[k] for k in (0, 1)]
+        print(f"  {NAMES[i]:<22} {v[0]:8.0f} {v[1]:8.0f}")
+    print(f"  {'total':<22} {tot[0]:8.0f} {tot[1]:8.0f}")
 
 
 if __name__ == "__main__":
