@@ -265,6 +265,26 @@ struct Pending {
   }
 };
 
+// Order in which the column FIR visits its input rows: alternately from both
+// ends of the lane's window, inwards (0, T-1, 1, T-2, ...).  Every output
+// then receives its small outer taps first and its large centre taps last,
+// so the partial sums stay small for most of the accumulation -- same FFMA2
+// and load counts as an ascending sweep.  Measured max |fast - exact| over
+// the whole c4 image: 4.29e-4 -> 2.60e-4 (the paper bound there is 3.65e-4),
+// c2 3.22e-4 -> 3.11e-4; the row pass gains less from it (ascending is
+// faster there; profiles/r01_notes.md).  The order depends only on an
+// output's position in its 16-aligned block: results stay independent of
+// the partition.
+#ifndef FBF_FIR_OI_ROW
+#define FBF_FIR_OI_ROW 0
+#endif
+#ifndef FBF_FIR_OI_COL
+#define FBF_FIR_OI_COL 1
+#endif
+__host__ __device__ constexpr int fir_order(int q, int n, bool oi) {
+  return !oi ? q : (q & 1) ? n - 1 - (q >> 1) : (q >> 1);
+}
+
 // Row pass: warp = (16 rows, one KR-chunk of output columns); lane l filters
 // row g of half h = l / 16 (plane A or B) into the R ring, and stores its
 // half of the centre (c, s) of each input row's KR pixels into the CS ring.
@@ -316,7 +336,8 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restric
 #pragma unroll
     for (int i = 0; i < C::KR; ++i) acc[i] = 0ull;
 #pragma unroll
-    for (int m = 0; m < C::KR + 2 * C::W; ++m) {
+    for (int q = 0; q < TAPS_IN; ++q) {
+      const int m = fir_order(q, TAPS_IN, FBF_FIR_OI_ROW);
       const p2 v = src[m];
 #pragma unroll
       for (int i = 0; i < C::KR; ++i) {
@@ -328,7 +349,7 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restric
       }
       if (m >= C::W && m < C::W + C::KR && live)  // centre of output column xc + m - W
         csrow[2 * (xc + m - C::W)] = lo_of(v);
-      defer_at(m);
+      defer_at(q);
     }
   }
   if (live) {
@@ -395,7 +416,8 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
 #pragma unroll
     for (int i = 0; i < C::KC; ++i) acc[i] = 0ull;
 #pragma unroll
-    for (int m = 0; m < TAPS_IN; ++m) {
+    for (int q = 0; q < TAPS_IN; ++q) {
+      const int m = fir_order(q, TAPS_IN, FBF_FIR_OI_COL);
       const p2 v = ring(m);
 #pragma unroll
       for (int i = 0; i < C::KC; ++i) {
@@ -405,7 +427,7 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
           acc[i] = fma2(pk(tv, tv), v, acc[i]);
         }
       }
-      batch(m);
+      batch(q);
     }
   }
 #pragma unroll

@@ -48,12 +48,10 @@ def test_paper_bound_at_full_size(name):
         return
     img = image_of(c)
     fast = fb.bilateral_fast(img, s, a)
-    if name == "c4":  # full-width strips: top edge, middle, bottom edge
-        for r0 in (0, c.height // 2 - 32, c.height - 64):
-            exact = fb.bilateral_exact_gpu(img, s, c.range_family, c.sigma_r, r0, 64)
-            err = np.abs(fast[r0:r0 + 64] - exact).max()
-            assert err <= bound, (r0, err, bound)
-        return
+    # whole image, c4 included (67 M pixels, 2,401 fp64 taps each: < 1 s on the
+    # GPU).  c4's bound (3.65e-4) is tight: a full-image check once caught a
+    # single noise-outlier pixel at 4.29e-4 before the column FIR visited its
+    # taps outside-in (profiles/r01_notes.md)
     exact = fb.bilateral_exact_gpu(img, s, c.range_family, c.sigma_r)
     err = np.abs(fast - exact).max()
     assert err <= bound, (err, bound)
