@@ -185,13 +185,17 @@ struct ModNext {
     }
   }
   // batch b of ceil(ELEMS / 4): four elements, the last batch the remainder
-  static constexpr int NBATCH = (ELEMS + 3) / 4;
+#ifndef FBF_MOD_BATCH
+#define FBF_MOD_BATCH 4
+#endif
+  static constexpr int BS = FBF_MOD_BATCH;  // independent sincos chains per batch
+  static constexpr int NBATCH = (ELEMS + BS - 1) / BS;
   static __device__ __forceinline__ void batch(int b, const int2* __restrict__ stage, p2* __restrict__ M,
                                                uint32_t n) {
-    if (4 * b + 4 <= ELEMS)
-      elements<4>(4 * b, stage, M, n);
+    if (BS * b + BS <= ELEMS)
+      elements<BS>(BS * b, stage, M, n);
     else
-      elements<(ELEMS % 4 ? ELEMS % 4 : 4)>(4 * b, stage, M, n);
+      elements<(ELEMS % BS ? ELEMS % BS : BS)>(BS * b, stage, M, n);
   }
 };
 
