@@ -248,6 +248,11 @@ struct PhaseClock {
 // (loads -> multiply -> shuffle -> add -> store) no longer stalls both warps of
 // an SMSP at the end of every column pass.  Divide steps (last harmonic) and a
 // unit's last step finish immediately.
+#ifndef FBF_DEFER_Q0
+#define FBF_DEFER_Q0 8
+#endif
+constexpr int kDeferQ0 = FBF_DEFER_Q0;  // first row-pass input position of the deferred finishes
+
 template <class C>
 struct Pending {
   static constexpr int KH = C::KC / 2;
@@ -310,7 +315,7 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restric
   auto defer_at = [&](int m) {  // finish pending row k at input position m (compile-time)
 #pragma unroll
     for (int k = 0; k < Pending<C>::KH; ++k)
-      if (C::DEFER && m == k * TAPS_IN / Pending<C>::KH) pd.finish(k, h, A.pq_cols);
+      if (C::DEFER && m == kDeferQ0 + k * (TAPS_IN - kDeferQ0) / Pending<C>::KH) pd.finish(k, h, A.pq_cols);
   };
   const int rel = a + g - base;
   const int slot = rel % C::RING;
