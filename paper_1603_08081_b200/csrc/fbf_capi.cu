@@ -820,8 +820,10 @@ int fbf_launches_per_call(const fbf_geometry* g, const fbf_filter* f, int varian
 // images of a batch, or row strips of one large image) issued alternately on
 // two streams, so chunk k's H2D / D2H copies overlap the kernels of its
 // neighbours.  Row strips carry their W halo rows (mirror only at the global
-// edges) and are cut on multiples of 16 rows: the fused kernel's results do
-// not depend on the cut (tests/test_gpu_device.py), so K only changes speed.
+// edges) and are cut on multiples of 16 rows.  A strip run with the whole
+// call's harmonic grouping reproduces one launch bit for bit; with its own
+// grouping (the default, see below) it agrees to fp32 rounding of the group
+// sums (tests/test_gpu_device.py).
 // Batches: up to 8 image chunks.  One image: K strips from a measured cost
 // model (plan_chunks).
 namespace {
@@ -856,14 +858,17 @@ std::vector<Chunk> plan_chunks(const fbf_geometry* g, int W, int variant) {
   // one image: K strips cost ~ a + b/K + c*K (b: the copies a strip pipeline
   // hides, c: per-strip prologue rows, launch and tail); fitted on c2 / c4
   // (profiles/r01_notes.md): K ~ sqrt(b/c) ~ sqrt(pixels / 0.45 M), at most 4
-  int best = static_cast<int>(std::lround(std::sqrt(px / 0.45e6)));
+  // (per-chunk harmonic groups make the short edge strips cheap: c2 measured
+  // best at K = 4 with 35 % edges, 1.45 -> 1.31 ms; c4 keeps K = 4 / 20 %)
+  int best = static_cast<int>(std::lround(std::sqrt(px / 0.3e6)));
   best = std::max(1, std::min(best, 4));
   if (const char* force = getenv("FBF_HOST_CHUNKS")) best = std::max(1, atoi(force));  // experiments
   while (best > 1 && g->out_rows / best < 4 * W + 16) --best;
   // the first strip's H2D and the last strip's D2H are not hidden: those two
   // strips get 20 % of a middle strip's rows (measured: c2 K=3 2553 -> 2730,
   // c4 K=4 1637 -> 1707 e2e Mpixel/s; FBF_HOST_EDGE overrides, experiments)
-  const long long e = best >= 3 ? (getenv("FBF_HOST_EDGE") ? atoi(getenv("FBF_HOST_EDGE")) : 20) : 100;
+  const long long e_default = px <= 16e6 ? 35 : 20;
+  const long long e = best >= 3 ? (getenv("FBF_HOST_EDGE") ? atoi(getenv("FBF_HOST_EDGE")) : e_default) : 100;
   const long long wsum = 2 * e + 100LL * (best - 2);
   auto cut = [&](int i) {  // cumulative weight of strips [0, i)
     const long long w = i == 0 ? 0 : i == best ? wsum : e + 100LL * (i - 1);
@@ -968,11 +973,17 @@ int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const fl
     gc.dst_bstride = db;
     return gc;
   };
-  // every chunk uses the harmonic grouping of the whole call (bit-identical to one launch)
+  // Each chunk picks its own harmonic grouping from the cost model (short edge
+  // strips: more groups, so their kernels finish while the middle strip's
+  // copies run).  A chunk whose count differs from the whole call's sums its
+  // group planes in another order: equal to one launch to fp32 rounding, not
+  // bit for bit.  FBF_HOST_INHERIT_GROUPS=1 restores the whole call's count
+  // for every chunk (bit-identical to one launch).
+  static const bool inherit = getenv("FBF_HOST_INHERIT_GROUPS") != nullptr;
   struct GroupsOverride {
     explicit GroupsOverride(int g) { g_groups_override = g; }
     ~GroupsOverride() { g_groups_override = 0; }
-  } groups_override(harmonic_groups(g, f->radius, f->N + 1));
+  } groups_override(inherit ? harmonic_groups(g, f->radius, f->N + 1) : 0);
   size_t ws_bytes = 0;
   for (const Chunk& c : chunks) {
     const fbf_geometry gc = chunk_geometry(c);

@@ -72,10 +72,13 @@ def test_device_path_matches_host_path():
 
 
 @pytest.mark.parametrize("shape", [(1536, 2048), (3, 1024, 1024), (4096, 1024)])
-def test_pipelined_host_path_is_bit_identical(shape):
+def test_pipelined_host_path_matches_one_launch(shape):
     """fbf_bilateral_fast_host cuts > 2 Mpx calls into row strips (one image) or
-    image chunks (batches) on two streams so the copies overlap the kernels;
-    the result must not depend on the cut."""
+    image chunks (batches) on two streams so the copies overlap the kernels.
+    Each chunk picks its own harmonic grouping, so a chunk whose group count
+    differs from one launch's sums its group planes in another order: the
+    result equals one launch to fp32 rounding (bit for bit where the counts
+    agree; FBF_HOST_INHERIT_GROUPS=1 forces that everywhere)."""
     c = CONFIGS["c2"]
     s, a = spatial_of(c), approx_of(c)
     rng = np.random.default_rng(sum(shape))
@@ -83,7 +86,7 @@ def test_pipelined_host_path_is_bit_identical(shape):
     batch = 1 if len(shape) == 2 else shape[0]
     h, w = shape[-2], shape[-1]
     dev = run_device(img.reshape(batch, h, w), fb.whole_geometry(w, h, batch), s, a).reshape(shape)
-    assert np.array_equal(dev, fb.bilateral_fast(img, s, a))
+    assert np.abs(dev - fb.bilateral_fast(img, s, a)).max() <= 2e-4
 
 
 def test_pipelined_host_path_reports_the_first_collapse():
