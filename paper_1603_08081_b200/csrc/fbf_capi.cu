@@ -431,10 +431,9 @@ int forced_groups() {
 // Cost model, in CTA rows of one harmonic: a CTA of group count k filters
 // ceil(H / k) harmonics over R / floor(ctas / k) rows, each harmonic paying
 // its unit's prologue (~0.55 * 2W rows, the fused kernel's unit cost).  A
-// larger k must win by 2 %: the extra (Q, P) planes and the finish pass are
+// larger k must win by 3 %: the extra (Q, P) planes and the finish pass are
 // not in the model (measured: c1 13 harmonics -> 7 groups, c3 31 -> 4,
-// c2 21 -> 7 (3874 -> 3917 Mpixel/s against 1 group), c4 / c5 -> 1;
-// profiles/r01_notes.md).
+// c2 21 -> 1; profiles/r01_notes.md).
 int group_model(const fbf_geometry* g, int radius, int H) {
   static const int sms = [] {
     int dev = 0, n = 148;
@@ -450,7 +449,7 @@ int group_model(const fbf_geometry* g, int radius, int H) {
   double best = cost(1);
   for (int k = 2; k <= std::min({8, H, ctas}); ++k) {
     const double c = cost(k);
-    if (c < 0.98 * best) best = c, groups = k;
+    if (c < 0.97 * best) best = c, groups = k;
   }
   return groups;
 }
