@@ -834,10 +834,18 @@ struct Chunk {
   int s0, s1;     // source rows (global) [s0, s1) held on the device for this chunk
 };
 
+// calls below this many pixels run as one launch (CUDA-graph replayed); from
+// 1 Mpixel on, two strips already hide half the copies (c3 1024^2 e2e
+// 0.404 -> 0.36 ms, tools/e2e_probe.py); FBF_HOST_MIN_MPX overrides (experiments)
+double pipeline_min_px() {
+  static const double v = getenv("FBF_HOST_MIN_MPX") ? atof(getenv("FBF_HOST_MIN_MPX")) * 1e6 : 1.0e6;
+  return v;
+}
+
 std::vector<Chunk> plan_chunks(const fbf_geometry* g, int W, int variant) {
   std::vector<Chunk> c;
   const double px = static_cast<double>(g->width) * g->out_rows * g->batch;
-  if (variant != FBF_VARIANT_FUSED || px < 2.0e6) {  // small: one launch
+  if (variant != FBF_VARIANT_FUSED || px < pipeline_min_px()) {  // small: one launch
     c.push_back({0, g->batch, g->out_row0, g->out_row0 + g->out_rows, g->src_row0, g->src_row0 + g->src_rows});
     return c;
   }

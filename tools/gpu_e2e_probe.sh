@@ -1,6 +1,7 @@
 #!/bin/bash
-# host-entry e2e after the per-chunk grouping change: default vs inherited groups, c2 / c4 / c5
-for cfg in c2 c4; do
-  FBF_HOST_INHERIT_GROUPS=1 python tools/e2e_probe.py $cfg
+# e2e of ~1 Mpixel calls: single CUDA-graph launch vs the two-stream strip pipeline
+for cfg in c3 c1; do
   python tools/e2e_probe.py $cfg
+  FBF_HOST_MIN_MPX=0.2 python tools/e2e_probe.py $cfg
+  FBF_HOST_MIN_MPX=0.2 FBF_HOST_CHUNKS=3 python tools/e2e_probe.py $cfg
 done
