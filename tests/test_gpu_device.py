@@ -73,7 +73,7 @@ def test_device_path_matches_host_path():
 
 @pytest.mark.parametrize("shape", [(1536, 2048), (3, 1024, 1024), (4096, 1024)])
 def test_pipelined_host_path_matches_one_launch(shape):
-    """fbf_bilateral_fast_host cuts > 2 Mpx calls into row strips (one image) or
+    """fbf_bilateral_fast_host cuts >= 1 Mpx calls into row strips (one image) or
     image chunks (batches) on two streams so the copies overlap the kernels.
     Each chunk picks its own harmonic grouping, so a chunk whose group count
     differs from one launch's sums its group planes in another order: the

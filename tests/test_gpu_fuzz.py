@@ -1,6 +1,6 @@
 """GPU: randomized geometries against the fp64 oracle -- image sizes, batches,
 Gaussian / box radii, harmonic counts, strip sub-geometries (device entry) and
-the pipelined host entry (> 2 Mpixel) -- to catch edge cases of the lane
+the pipelined host entry (>= 1 Mpixel) -- to catch edge cases of the lane
 mappings, rings and chunking that the fixed configs do not reach."""
 import numpy as np
 import pytest
@@ -46,7 +46,7 @@ def test_random_geometries(oracle, seed):
 
 @pytest.mark.parametrize("seed", range(4))
 def test_random_large_pipelined(oracle, seed):
-    """> 2 Mpixel calls: the host entry's strip / image-chunk pipeline"""
+    """>= 1 Mpixel calls: the host entry's strip / image-chunk pipeline"""
     rng = np.random.default_rng(100 + seed)
     h, w = int(rng.integers(1100, 2100)), int(rng.integers(1100, 2100))
     s = fb.make_spatial_gaussian(float(rng.choice([1.0, 2.5, 5.0])))
