@@ -420,6 +420,13 @@ struct Layout {
 // (results independent of the pipeline cut): set around its chunk launches
 thread_local int g_groups_override = 0;
 
+// longest row run a CTA filters per sweep over the harmonics (FBF_SEG_MAX,
+// experiments; default unlimited)
+int seg_max_rows() {
+  static const int v = getenv("FBF_SEG_MAX") ? std::max(16, atoi(getenv("FBF_SEG_MAX"))) : (1 << 30);
+  return v;
+}
+
 int forced_groups() {
   static const int forced = [] {
     const char* e = getenv("FBF_GROUPS");
@@ -682,7 +689,7 @@ int fbf_filter_prepared_device(const fbf_geometry* gp, const fbf_filter* f, floa
     A.dst = dst;
     A.pq = P.pq;
     A.bad = d_bad;
-    A.seg_max = 1 << 30;
+    A.seg_max = seg_max_rows();
     cudaError_t e = cudaSuccess;
     const int groups = launch_fused_range(A, f, 0, P.H.N + 1, harmonic_groups(gp, f->radius, P.H.N + 1), false, st, &e);
     FBF_CUDA(e);
@@ -752,7 +759,7 @@ int fbf_partial_sums_device(const fbf_geometry* gp, const fbf_filter* f, int n_l
     A.k = P.K;
     A.uf = P.uf;
     A.pq = P.pq;
-    A.seg_max = 1 << 30;
+    A.seg_max = seg_max_rows();
     cudaError_t e = cudaSuccess;
     const int groups = launch_fused_range(A, f, n_lo, n_hi, harmonic_groups(gp, f->radius, n_hi - n_lo), true, st, &e);
     FBF_CUDA(e);
