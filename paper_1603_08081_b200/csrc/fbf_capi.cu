@@ -856,8 +856,9 @@ std::vector<Chunk> plan_chunks(const fbf_geometry* g, int W, int variant) {
     c.push_back({0, g->batch, g->out_row0, g->out_row0 + g->out_rows, g->src_row0, g->src_row0 + g->src_rows});
     return c;
   }
-  if (g->batch >= 2) {  // whole images per chunk; the first and last chunk at 20 % weight
-    const int k = std::min(g->batch, 8);
+  if (g->batch >= 2) {  // whole images per chunk (up to 16: c5 e2e 5320 -> 5529 against 8); first and last chunk at 20 % weight
+    static const int kmax = getenv("FBF_HOST_BATCH_CHUNKS") ? std::max(2, atoi(getenv("FBF_HOST_BATCH_CHUNKS"))) : 16;
+    const int k = std::min(g->batch, std::min(kmax, 16));  // 16: the pipeline's chunk limit
     const long long e = k >= 3 ? 20 : 100, wsum = 2 * e + 100LL * (k - 2);
     auto cut = [&](int i) {
       const long long w = i == 0 ? 0 : i == k ? wsum : e + 100LL * (i - 1);

@@ -1,7 +1,5 @@
 #!/bin/bash
-# e2e of ~1 Mpixel calls: single CUDA-graph launch vs the two-stream strip pipeline
-for cfg in c3 c1; do
-  python tools/e2e_probe.py $cfg
-  FBF_HOST_MIN_MPX=0.2 python tools/e2e_probe.py $cfg
-  FBF_HOST_MIN_MPX=0.2 FBF_HOST_CHUNKS=3 python tools/e2e_probe.py $cfg
+# batch pipeline chunk count (c5, 256 images): e2e through the host entry
+for k in 8 12 16; do
+  FBF_HOST_BATCH_CHUNKS=$k python bench.py --config c5 --steps 5 --warmup 3 --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('chunks=$k', round(d['value']), round(d['e2e']['value']))"
 done
