@@ -1,5 +1,5 @@
 #!/bin/bash
-# batch pipeline chunk count (c5, 256 images): e2e through the host entry
-for k in 8 12 16; do
-  FBF_HOST_BATCH_CHUNKS=$k python bench.py --config c5 --steps 5 --warmup 3 --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('chunks=$k', round(d['value']), round(d['e2e']['value']))"
-done
+# c4 (8192^2) strip pipeline: strip count x edge weight
+python tools/e2e_probe.py c4
+for k in 6 8; do for e in 10 20; do FBF_HOST_CHUNKS=$k FBF_HOST_EDGE=$e python tools/e2e_probe.py c4; done; done
+FBF_HOST_CHUNKS=4 FBF_HOST_EDGE=10 python tools/e2e_probe.py c4
