@@ -100,41 +100,68 @@ int fbf_filter_prepared_device(const fbf_geometry* g, const fbf_filter* f, float
                                unsigned long long* d_bad, int variant, void* stream);
 /* Harmonic groups (CTA groups splitting the harmonics, each with its own
  * (Q, P) plane) the fused path uses for this geometry, radius and order N.
- * Calls on different geometries (e.g. row strips of one image) with different
- * group counts agree to fp32 rounding of the group sums, not bit for bit. */
+ * Every harmonic term is rounded once to a fixed-point grid and summed as an
+ * integer, so the result is the same bits for any group count, strip or
+ * batch partition, pipeline chunking or GPU split. */
 int fbf_harmonic_groups(const fbf_geometry* g, int radius, int N);
 /* Kernel launches one fbf_bilateral_fast_device call makes. */
 int fbf_launches_per_call(const fbf_geometry* g, const fbf_filter* f, int variant);
 
 /* Harmonic split (SURVEY.md §8(e) optional mode): the partial numerator and
  * denominator sums over harmonics [n_lo, n_hi) into pq_out, a dense device
- * array of (Q, P) fp32 pairs (batch x out_rows x width), after
- * fbf_prepare_device on the same workspace.  Ranks holding disjoint harmonic
- * ranges sum their pq_out (e.g. NCCL all-reduce) and call fbf_finish_device,
- * which divides (with the reference's collapse check) into dst. */
+ * array of (Q, P) fp64 pairs (batch x out_rows x width), after
+ * fbf_prepare_device on the same workspace.  The values are exact multiples of
+ * the call's fixed-point grid, so partial planes of disjoint harmonic ranges
+ * sum exactly in any order (e.g. an NCCL fp64 all-reduce) to the bits of a
+ * single-GPU call; fbf_finish_device then divides (with the reference's
+ * collapse check) into dst. */
 int fbf_partial_sums_device(const fbf_geometry* g, const fbf_filter* f, int n_lo, int n_hi,
-                            float* pq_out, void* workspace, size_t workspace_bytes, int variant,
+                            double* pq_out, void* workspace, size_t workspace_bytes, int variant,
                             void* stream);
-int fbf_finish_device(const fbf_geometry* g, const fbf_filter* f, const float* pq, float* dst,
+int fbf_finish_device(const fbf_geometry* g, const fbf_filter* f, const double* pq, float* dst,
                       unsigned long long* d_bad, void* stream);
 
-/* Synchronous, host buffers (fp32): H2D, filter, D2H.  On FBF_EANOMALY
- * *bad_index holds the first offending index. */
+/* Synchronous, host buffers (fp32): H2D, filter, D2H, pipelined in chunks
+ * on two streams from 1 Mpixel.  On FBF_EANOMALY *bad_index holds the first
+ * offending index. */
 int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const float* src,
                             float* dst, int variant, long long* bad_index);
 
-/* The host entry points reuse one stream and one device buffer per calling
- * thread; this frees the calling thread's. */
+/* The host entry points keep one context per calling thread and device
+ * (streams, a grow-only device buffer, pinned staging, a cached graph); this
+ * frees the calling thread's (they are also freed when the thread exits). */
 void fbf_release_host_buffers(void);
 
-/* Same on fp64 host buffers (the reference Image stores doubles). */
+/* Same on fp64 host buffers (the reference Image stores doubles): the
+ * double <-> float conversions run on a host thread pool into pinned staging,
+ * overlapped chunk by chunk with the GPU pipeline. */
 int fbf_bilateral_fast_host_f64(const fbf_geometry* g, const fbf_filter* f, const double* src,
                                 double* dst, int variant, long long* bad_index);
 
-/* convolve (spatial.hpp:98-112), direct backend, fp32 on the device. */
+/* One call over several GPUs of the box (devices[0..ndevices-1]), one host
+ * worker thread per device: a batch is split by whole images, a single image
+ * by row strips (16-row aligned cuts, each strip with its W halo rows; mirror
+ * padding only at the global edges).  No exchange between devices; the result
+ * equals the single-device call bit for bit. */
+int fbf_bilateral_fast_host_multi(const fbf_geometry* g, const fbf_filter* f, const float* src,
+                                  float* dst, int variant, long long* bad_index,
+                                  const int* devices, int ndevices);
+int fbf_bilateral_fast_host_multi_f64(const fbf_geometry* g, const fbf_filter* f,
+                                      const double* src, double* dst, int variant,
+                                      long long* bad_index, const int* devices, int ndevices);
+
+/* convolve (spatial.hpp:98-112), direct backend: out(i) = sum_j profile[j+W]
+ * in(i-j) along rows then columns, mirror boundaries, any radius.  Device
+ * entry points in fp32 and fp64 (workspace: fbf_convolve_workspace_bytes);
+ * the host entry is fp64 on the device, in the reference's summation order
+ * (bit-identical to the reference). */
+size_t fbf_convolve_workspace_bytes(int width, int height, int radius);
 int fbf_convolve_device(int width, int height, const double* profile, int radius,
                         const float* src, float* dst, void* workspace, size_t workspace_bytes,
                         void* stream);
+int fbf_convolve_device_f64(int width, int height, const double* profile, int radius,
+                            const double* src, double* dst, void* workspace,
+                            size_t workspace_bytes, void* stream);
 int fbf_convolve_host_f64(int width, int height, const double* profile, int radius,
                           const double* src, double* dst);
 /* convolve with the recursive backend: the IIR Gaussian of sigma (fp64; the
@@ -147,6 +174,11 @@ int fbf_convolve_recursive_host_f64(int width, int height, double sigma, const d
  * dst: fp64 rows [out_row0, out_row0+out_rows); batch must be 1. */
 int fbf_bilateral_exact_device(const fbf_geometry* g, const double* profile, int radius, int family,
                                double sigma_r, const float* src, double* dst, void* stream);
+
+/* bilateral_exact of a whole fp64 host image, Gaussian or exponential range
+ * kernel (the C++ API's bilateral_exact for those families; radius <= 64). */
+int fbf_bilateral_exact_host_f64(int width, int height, const double* profile, int radius, int family,
+                                 double sigma_r, const double* src, double* dst);
 
 /* local_dynamic_range (bilateral.hpp:21-74) on the device, fp64 (exact):
  * *T = ceil(max over pixels of windowed max - windowed min). */

@@ -4,6 +4,9 @@
                   (oracle/fbf_oracle.c) of the reference path.
 * ``Reference`` : oracle/_ref/libfbf_ref.so, the UNMODIFIED reference headers
                   compiled in place (oracle/ref_shim.cpp + oracle/Makefile).
+* ``synth_image``: oracle/_synth/libfbf_synth.so, the BASELINE input generator
+                  built from the product's own generator source, so the
+                  reference arm of bench.py never loads the product library.
 
 Only tests/, __graft_entry__.smoke() and bench.py's CPU legs may import this
 module; the product package never does.
@@ -19,6 +22,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "libfbf_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libfbf_ref.so")
+SYNTH_SO = os.path.join(HERE, "_synth", "libfbf_synth.so")
 
 _D = ctypes.POINTER(ctypes.c_double)
 _I = ctypes.POINTER(ctypes.c_int)
@@ -306,3 +310,26 @@ class Reference:
                                                _dp(out)):
             raise ValueError(self.last_error())
         return out
+
+
+_SYNTH = None
+
+
+def synth_image(seed, width, height, rects, noise, row0=0, rows=None, nthreads=None):
+    """fbf_synth_image from oracle/_synth/libfbf_synth.so -> float32 array (rows x width)."""
+    global _SYNTH
+    if _SYNTH is None:
+        if not os.path.exists(SYNTH_SO):
+            build()
+        L = ctypes.CDLL(SYNTH_SO)
+        L.fbf_synth_image.argtypes = [ctypes.c_ulonglong, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                      ctypes.POINTER(ctypes.c_float), ctypes.c_int]
+        _SYNTH = L
+    rows = height - row0 if rows is None else rows
+    out = np.empty((rows, width), dtype=np.float32)
+    rc = _SYNTH.fbf_synth_image(seed, width, height, rects, noise, row0, rows,
+                                out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), nthreads or os.cpu_count() or 1)
+    if rc:
+        raise ValueError("fbf_synth_image: invalid arguments")
+    return out

@@ -78,6 +78,13 @@ SIGNATURES = {
     "fbf_convolve_device": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _D, ctypes.c_int, _P, _P, _P,
                                            ctypes.c_size_t, _P]),
     "fbf_convolve_host_f64": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _D, ctypes.c_int, _D, _D]),
+    "fbf_convolve_device_f64": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _D, ctypes.c_int, _P, _P, _P,
+                                               ctypes.c_size_t, _P]),
+    "fbf_convolve_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "fbf_bilateral_fast_host_multi": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.POINTER(Filter), _F, _F,
+                                                     ctypes.c_int, _LL, _I, ctypes.c_int]),
+    "fbf_bilateral_fast_host_multi_f64": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.POINTER(Filter), _D, _D,
+                                                         ctypes.c_int, _LL, _I, ctypes.c_int]),
     "fbf_convolve_recursive_host_f64": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_double, _D, _D]),
     "fbf_harmonic_groups": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.c_int, ctypes.c_int]),
     "fbf_spatial_gaussian": (ctypes.c_int, [ctypes.c_double, _D, _I, _D]),
@@ -92,6 +99,8 @@ SIGNATURES = {
     "fbf_probe_fma_peak": (ctypes.c_int, [_D, _D, _P]),
     "fbf_release_host_buffers": (None, []),
     "fbf_local_dynamic_range_host_f64": (ctypes.c_int, [_D, ctypes.c_int, ctypes.c_int, ctypes.c_int, _I]),
+    "fbf_bilateral_exact_host_f64": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _D, ctypes.c_int, ctypes.c_int,
+                                                    ctypes.c_double, _D, _D]),
     "fbf_bilateral_exact_device": (ctypes.c_int, [ctypes.POINTER(Geometry), _D, ctypes.c_int, ctypes.c_int,
                                                   ctypes.c_double, _P, _P, _P]),
 }
@@ -310,6 +319,34 @@ def bilateral_fast(image: np.ndarray, spatial: SpatialKernel, approx: FourierKer
     return out
 
 
+def bilateral_fast_multi(image: np.ndarray, spatial: SpatialKernel, approx: FourierKernelApprox,
+                         devices: Sequence[int], variant: str = "fused", check_epsilon: bool = True) -> np.ndarray:
+    """One call over several GPUs (fbf_bilateral_fast_host_multi[_f64]): row strips of one image or
+    images of a batch per device, one host worker thread per device; bit-identical to one device."""
+    a = np.asarray(image)
+    if a.size == 0:
+        raise ValueError("bilateral_fast: empty image")
+    batch = 1 if a.ndim == 2 else a.shape[0]
+    h, w = a.shape[-2], a.shape[-1]
+    g = whole_geometry(w, h, batch)
+    f = _filter_struct(spatial, approx, check_epsilon)
+    bad = ctypes.c_longlong(-1)
+    devs = (ctypes.c_int * len(devices))(*devices)
+    if a.dtype == np.float32:
+        src = np.ascontiguousarray(a)
+        out = np.empty_like(src)
+        rc = lib.fbf_bilateral_fast_host_multi(ctypes.byref(g), ctypes.byref(f), src.ctypes.data_as(_F),
+                                               out.ctypes.data_as(_F), _VARIANTS[variant], ctypes.byref(bad),
+                                               devs, len(devices))
+    else:
+        src = np.ascontiguousarray(a, dtype=np.float64)
+        out = np.empty_like(src)
+        rc = lib.fbf_bilateral_fast_host_multi_f64(ctypes.byref(g), ctypes.byref(f), _dp(src), _dp(out),
+                                                   _VARIANTS[variant], ctypes.byref(bad), devs, len(devices))
+    _check(rc)
+    return out
+
+
 def bilateral_fast_device(src_ptr: int, dst_ptr: int, geometry: Geometry, spatial: SpatialKernel,
                           approx: FourierKernelApprox, workspace_ptr: int, workspace_bytes: int,
                           bad_ptr: int, stream: int = 0, variant: str = "fused",
@@ -347,7 +384,9 @@ def launches_per_call(geometry: Geometry, spatial: SpatialKernel, approx: Fourie
 def partial_sums_device(pq_ptr: int, geometry: Geometry, spatial: SpatialKernel, approx: FourierKernelApprox,
                         n_lo: int, n_hi: int, workspace_ptr: int, workspace_bytes: int, stream: int = 0,
                         variant: str = "fused", check_epsilon: bool = True) -> None:
-    """(Q, P) partial sums over harmonics [n_lo, n_hi) into a dense float2 device array (after prepare_device)."""
+    """(Q, P) partial sums over harmonics [n_lo, n_hi) into a dense fp64-pair device array (after
+    prepare_device): exact multiples of the call's fixed-point grid, so partial planes of disjoint
+    harmonic ranges sum exactly, in any order, to the single-call values."""
     f = _filter_struct(spatial, approx, check_epsilon)
     _check(lib.fbf_partial_sums_device(ctypes.byref(geometry), ctypes.byref(f), int(n_lo), int(n_hi), pq_ptr,
                                        workspace_ptr, workspace_bytes, _VARIANTS[variant], stream))
@@ -355,7 +394,7 @@ def partial_sums_device(pq_ptr: int, geometry: Geometry, spatial: SpatialKernel,
 
 def finish_device(pq_ptr: int, dst_ptr: int, geometry: Geometry, spatial: SpatialKernel,
                   approx: FourierKernelApprox, bad_ptr: int, stream: int = 0, check_epsilon: bool = True) -> None:
-    """Divide summed (Q, P) into the output with the reference's denominator-collapse check."""
+    """Divide summed fp64 (Q, P) pairs into the output with the reference's denominator-collapse check."""
     f = _filter_struct(spatial, approx, check_epsilon)
     _check(lib.fbf_finish_device(ctypes.byref(geometry), ctypes.byref(f), pq_ptr, dst_ptr, bad_ptr, stream))
 

@@ -1,7 +1,9 @@
-// fbf_capi.cu -- the extern "C" boundary (include/fourierbf_b200.h) plus the
-// small kernels around the fused one: the phase prep, the naive multi-kernel
-// variant (HBM-resident planes), the standalone separable convolution and the
-// FP32 FMA-pipe peak probe used as the roofline denominator.
+// fbf_capi.cu -- the device-side extern "C" boundary (include/fourierbf_b200.h)
+// plus the small kernels around the fused one: the phase prep, the naive
+// multi-kernel variant (HBM-resident planes), the group sum / divide, the
+// standalone separable convolution (fp32 and fp64) and the FP32 FMA-pipe peak
+// probe used as the roofline denominator.  The host-buffer entry points
+// (pipelines, per-device contexts, multi-GPU) live in fbf_hostpath.cu.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -14,6 +16,7 @@
 #include "fbf_common.h"
 #include "fbf_device.cuh"
 #include "fbf_params.h"
+#include "fbf_tuning.h"
 #include "fourierbf_b200.h"
 
 namespace fbf {
@@ -40,129 +43,118 @@ size_t iir_workspace_bytes(const fbf_geometry* g, int radius);
 template <class Tin, class Tout>
 int iir_bilateral(const fbf_geometry* g, const fbf_filter* f, const Tin* src, Tout* dst, void* ws, size_t ws_bytes,
                   unsigned long long* d_bad, cudaStream_t st);
+// per-device SM count, cached (group model, launch shapes)
+void sm_count(int dev, int* sms) {
+  static int cache[64] = {};
+  *sms = 148;
+  if (dev >= 0 && dev < 64) {
+    if (!cache[dev]) cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev);
+    if (cache[dev] > 0) *sms = cache[dev];
+  }
+}
 }  // namespace fbf
 
 namespace {
-
-// The synchronous host entry points keep one stream and one grow-only device
-// buffer per calling thread (and device): no allocation, stream creation or
-// pool trimming inside repeated calls.  fbf_release_host_buffers() frees them.
-struct HostCtx {
-  int dev = -1;
-  cudaStream_t st = nullptr;   // chunk stream 0
-  cudaStream_t st2 = nullptr;  // chunk stream 1 (copies of one chunk overlap the kernels of the other)
-  cudaEvent_t ev[2] = {nullptr, nullptr};
-  cudaEvent_t join = nullptr;          // stream 1 back into stream 0
-  unsigned long long* h_bad = nullptr;  // pinned: per-chunk collapse indices (graph-capturable read-back)
-  char* buf = nullptr;
-  size_t cap = 0;
-  // the last call's work as a CUDA graph, replayed when the next call is the
-  // same (geometry, filter, buffers): one launch instead of ~10 API calls
-  std::vector<unsigned char> graph_key;
-  cudaGraphExec_t graph = nullptr;
-};
-thread_local HostCtx g_host;
-thread_local float* g_pinned = nullptr;  // fp32 staging for the fp64 entry points
-thread_local size_t g_pinned_cap = 0;
-
-int host_staging(size_t bytes, float*& out) {
-  if (g_pinned_cap < bytes) {
-    if (g_pinned) cudaFreeHost(g_pinned);
-    g_pinned = nullptr;
-    g_pinned_cap = 0;
-    FBF_CUDA(cudaMallocHost(reinterpret_cast<void**>(&g_pinned), bytes));
-    g_pinned_cap = bytes;
-  }
-  out = g_pinned;
-  return FBF_OK;
-}
-
-int host_ctx(size_t bytes, HostCtx*& out) {
-  int dev = 0;
-  FBF_CUDA(cudaGetDevice(&dev));
-  if (g_host.dev != dev) {  // first call on this thread, or the thread switched devices
-    g_host = HostCtx{};
-    g_host.dev = dev;
-    FBF_CUDA(cudaStreamCreateWithFlags(&g_host.st, cudaStreamNonBlocking));
-    FBF_CUDA(cudaStreamCreateWithFlags(&g_host.st2, cudaStreamNonBlocking));
-    for (auto& e : g_host.ev) FBF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    FBF_CUDA(cudaEventCreateWithFlags(&g_host.join, cudaEventDisableTiming));
-    FBF_CUDA(cudaMallocHost(reinterpret_cast<void**>(&g_host.h_bad), 16 * sizeof(unsigned long long)));
-  }
-  if (g_host.cap < bytes) {
-    if (g_host.buf) {
-      cudaStreamSynchronize(g_host.st);
-      cudaStreamSynchronize(g_host.st2);
-      if (g_host.graph) cudaGraphExecDestroy(g_host.graph);  // it names the old buffer
-      g_host.graph = nullptr;
-      g_host.graph_key.clear();
-      cudaFree(g_host.buf);
-      g_host.buf = nullptr;
-      g_host.cap = 0;
-    }
-    FBF_CUDA(cudaMalloc(reinterpret_cast<void**>(&g_host.buf), bytes));
-    g_host.cap = bytes;
-  }
-  out = &g_host;
-  return FBF_OK;
-}
 
 // ---------------------------------------------------------------------------
 // prep: (u, f') per source pixel.  u = round(f' * omega/(2 pi) * 2^32) mod 2^32
 // in fp64 (exact base phase in turns), f' = f - shift.
 
-__global__ void prep_kernel(const float* __restrict__ src, int2* __restrict__ uf, Geometry g,
-                            double turns_scaled, float shift) {
+// max |f'| of the call into the workspace header (fixed-point P grid,
+// fbf_params.h): one atomic per warp
+__device__ __forceinline__ void note_fmax(float m, unsigned* fmax) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(fmax, __float_as_uint(m));
+}
+
+__device__ __forceinline__ int2 phase_of(float f, double turns_scaled, float shift, float& m) {
+  const double fd = static_cast<double>(f) - static_cast<double>(shift);
+  const long long u = __double2ll_rn(fd * turns_scaled);
+  const float ff = static_cast<float>(fd);
+  m = fmaxf(m, fabsf(ff));
+  return make_int2(static_cast<int>(static_cast<unsigned>(u)), __float_as_int(ff));
+}
+
+// naive path: dense (u, f') of the source rows, batch x src_rows x width
+__global__ void prep_kernel(const float* __restrict__ src, int2* __restrict__ uf, Geometry g, double turns_scaled,
+                            float shift, unsigned* fmax) {
   const long long per = static_cast<long long>(g.src_rows) * g.width;
   const long long total = per * g.batch;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+  float m = 0.f;
+  for (long long i0 = blockIdx.x * static_cast<long long>(blockDim.x); i0 < total;
+       i0 += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = i0 + threadIdx.x;
+    if (i >= total) continue;
     const long long b = i / per;
     const long long r = i - b * per;
     const int y = static_cast<int>(r / g.width);
     const int x = static_cast<int>(r - static_cast<long long>(y) * g.width);
-    const float f = src[b * g.src_bstride + static_cast<long long>(y) * g.src_pitch + x];
-    const double fd = static_cast<double>(f) - static_cast<double>(shift);
-    const long long u = __double2ll_rn(fd * turns_scaled);
-    uf[i] = make_int2(static_cast<int>(static_cast<unsigned>(u)),
-                                                  __float_as_int(static_cast<float>(fd)));
+    uf[i] = phase_of(src[b * g.src_bstride + static_cast<long long>(y) * g.src_pitch + x], turns_scaled, shift, m);
   }
+  note_fmax(m, fmax);
 }
 
 // fused path: the same (u, f') on a mirror-padded grid, rows = global rows
 // [out_row0 - W, out_row0 + out_rows + W), columns = global [-W, cols + W)
 // with cols = strips * TW, so every TMA tile of the fused kernel is in bounds.
-// One block row per padded row (blockIdx.y) and image (blockIdx.z), two
-// columns per thread and one 16-byte store: no per-element index divisions.
-// Same per-element arithmetic as the dense prep (bit-identical phases).
-__global__ void prep_padded_kernel(const float* __restrict__ src, int2* __restrict__ uf, Geometry g,
-                                   int W, int cols, double turns_scaled, float shift) {
+// Grid: x = column blocks, y = (image, padded row) in a grid-stride loop (any
+// height or batch: no 65535 limit), two columns per thread and one 16-byte
+// store.  Same per-element arithmetic as the dense prep (bit-identical phases).
+__global__ void prep_padded_kernel(const float* __restrict__ src, int2* __restrict__ uf, Geometry g, int W, int cols,
+                                   double turns_scaled, float shift, unsigned* fmax) {
   const int pw = cols + 2 * W, ph = g.out_rows + 2 * W;
-  const int py = blockIdx.y, b = blockIdx.z;
-  const int gy = mirror_index(g.out_row0 - W + py, g.full_height) - g.src_row0;
-  const float* __restrict__ srow = src + b * g.src_bstride + static_cast<long long>(gy) * g.src_pitch;
-  int4* __restrict__ urow = reinterpret_cast<int4*>(uf + (static_cast<long long>(b) * ph + py) * pw);
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; 2 * q < pw; q += gridDim.x * blockDim.x) {
-    int v[4];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int gx = mirror_index(2 * q + e - W, g.width);
-      const double fd = static_cast<double>(srow[gx]) - static_cast<double>(shift);
-      const long long u = __double2ll_rn(fd * turns_scaled);
-      v[2 * e] = static_cast<int>(static_cast<unsigned>(u));
-      v[2 * e + 1] = __float_as_int(static_cast<float>(fd));
+  const long long nrows = static_cast<long long>(ph) * g.batch;
+  float m = 0.f;
+  for (long long r = blockIdx.y; r < nrows; r += gridDim.y) {
+    const int b = static_cast<int>(r / ph), py = static_cast<int>(r - static_cast<long long>(b) * ph);
+    const int gy = mirror_index(g.out_row0 - W + py, g.full_height) - g.src_row0;
+    const float* __restrict__ srow = src + b * g.src_bstride + static_cast<long long>(gy) * g.src_pitch;
+    int4* __restrict__ urow = reinterpret_cast<int4*>(uf + r * pw);
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; 2 * q < pw; q += gridDim.x * blockDim.x) {
+      const int2 a = phase_of(srow[mirror_index(2 * q - W, g.width)], turns_scaled, shift, m);
+      const int2 c = phase_of(srow[mirror_index(2 * q + 1 - W, g.width)], turns_scaled, shift, m);
+      urow[q] = make_int4(a.x, a.y, c.x, c.y);
     }
-    urow[q] = make_int4(v[0], v[1], v[2], v[3]);
   }
+  note_fmax(m, fmax);
+}
+
+// ---------------------------------------------------------------------------
+// Runtime-length taps (naive chain, standalone convolve): profile[0..2W] in the
+// workspace, any radius.  Uploaded by kernel parameters, kTapChunk at a time
+// (graph-capturable, no pageable copies).
+constexpr int kTapChunk = 2048;
+struct TapChunk {
+  int off, n;
+  double t[kTapChunk];
+};
+__global__ void store_taps(const __grid_constant__ TapChunk c, float* __restrict__ t32, double* __restrict__ t64) {
+  for (int i = threadIdx.x; i < c.n; i += blockDim.x) {
+    if (t32) t32[c.off + i] = static_cast<float>(c.t[i]);
+    if (t64) t64[c.off + i] = c.t[i];
+  }
+}
+cudaError_t upload_taps(const double* profile, int radius, float* t32, double* t64, cudaStream_t st) {
+  TapChunk c;
+  for (int off = 0; off < 2 * radius + 1; off += kTapChunk) {
+    c.off = off;
+    c.n = std::min(kTapChunk, 2 * radius + 1 - off);
+    std::memcpy(c.t, profile + off, sizeof(double) * c.n);
+    store_taps<<<1, 256, 0, st>>>(c, t32, t64);
+  }
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
 // naive variant: per harmonic four kernels over HBM-resident float4 planes
 //   modulate -> row FIR -> column FIR -> demodulate, then one divide kernel.
+// out(i) = sum_j profile[j+W] in(i-j), ascending j (spatial.hpp:74-89).
 
 struct NaiveArgs {
   Geometry g;  // uf / planes use a dense layout: batch x src_rows x width
-  Taps k;
+  int W;
+  const float* taps;  // profile[0..2W] (workspace)
 };
 
 __global__ void naive_modulate(const int2* __restrict__ uf, ulonglong2* __restrict__ M, long long total,
@@ -181,15 +173,15 @@ __global__ void naive_rows(const ulonglong2* __restrict__ in, ulonglong2* __rest
                            const __grid_constant__ NaiveArgs a) {
   const long long per = static_cast<long long>(a.g.src_rows) * a.g.width;
   const long long total = per * a.g.batch;
-  const int W = a.k.W;
+  const int W = a.W;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long rowbase = i - (i % a.g.width);
     const int x = static_cast<int>(i % a.g.width);
     p2 A = 0, B = 0;
-    for (int j = -W; j <= W; ++j) {  // out(x) = sum_j p[j] in(x - j), spatial.hpp:82-86
+    for (int j = -W; j <= W; ++j) {
       const ulonglong2 v = in[rowbase + mirror_index(x - j, a.g.width)];
-      const float tv = a.k.t[j < 0 ? -j : j];
+      const float tv = a.taps[j + W];
       A = fma2(pk(tv, tv), v.x, A);
       B = fma2(pk(tv, tv), v.y, B);
     }
@@ -202,7 +194,7 @@ __global__ void naive_cols(const ulonglong2* __restrict__ in, ulonglong2* __rest
   const long long per_out = static_cast<long long>(a.g.out_rows) * a.g.width;
   const long long per_src = static_cast<long long>(a.g.src_rows) * a.g.width;
   const long long total = per_out * a.g.batch;
-  const int W = a.k.W;
+  const int W = a.W;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long b = i / per_out;
@@ -214,7 +206,7 @@ __global__ void naive_cols(const ulonglong2* __restrict__ in, ulonglong2* __rest
     for (int j = -W; j <= W; ++j) {
       const int sy = mirror_index(y - j, a.g.full_height) - a.g.src_row0;
       const ulonglong2 v = src[static_cast<long long>(sy) * a.g.width + x];
-      const float tv = a.k.t[j < 0 ? -j : j];
+      const float tv = a.taps[j + W];
       A = fma2(pk(tv, tv), v.x, A);
       B = fma2(pk(tv, tv), v.y, B);
     }
@@ -223,7 +215,10 @@ __global__ void naive_cols(const ulonglong2* __restrict__ in, ulonglong2* __rest
 }
 
 __global__ void naive_demod(const ulonglong2* __restrict__ M, const ulonglong2* __restrict__ C,
-                            p2* __restrict__ pq, Geometry g, float dn, int first) {
+                            p2* __restrict__ pq, Geometry g, float dn, int first, int aq,
+                            const unsigned* __restrict__ fmax) {
+  const FixedScale fs = fixed_scale(aq, fmax);
+  const p2 dd = pk(dn * fs.sq, dn * fs.sp);
   const long long per_out = static_cast<long long>(g.out_rows) * g.width;
   const long long per_src = static_cast<long long>(g.src_rows) * g.width;
   const long long total = per_out * g.batch;
@@ -238,12 +233,18 @@ __global__ void naive_demod(const ulonglong2* __restrict__ M, const ulonglong2* 
     const float cc = lo_of(m.x), ss = lo_of(m.y);
     p2 qp = mul2(pk(cc, cc), c.x);  // (c Gc, c Fc) + (s Gs, s Fs)
     qp = fma2(pk(ss, ss), c.y, qp);
-    pq[i] = first ? mul2(pk(dn, dn), qp) : fma2(pk(dn, dn), qp, pq[i]);
+    const p2 t = to_fixed(mul2(dd, qp));  // fixed-point term (fbf_params.h)
+    pq[i] = first ? t : iadd2(pq[i], t);
   }
 }
 
-__global__ void finish_kernel(const p2* __restrict__ pq, float* __restrict__ dst, Geometry g,
-                              float shift, float q_floor, unsigned long long* bad) {
+// divide with the collapse check (bilateral.hpp:147-158); pq: fixed-point
+// int32 pairs (fbf_params.h), or exact fp64 (Q, P) pairs (pq64: the summed
+// output of fbf_partial_sums_device, fbf_finish_device)
+__global__ void finish_kernel(const p2* __restrict__ pq, const double2* __restrict__ pq64, float* __restrict__ dst,
+                              Geometry g, float shift, float q_floor, unsigned long long* bad, int aq,
+                              const unsigned* __restrict__ fmax) {
+  const FixedScale fs = fixed_scale(aq, fmax);
   const long long per_out = static_cast<long long>(g.out_rows) * g.width;
   const long long total = per_out * g.batch;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -253,7 +254,13 @@ __global__ void finish_kernel(const p2* __restrict__ pq, float* __restrict__ dst
     const int yl = static_cast<int>(r / g.width);
     const int x = static_cast<int>(r % g.width);
     float Q, P;
-    upk(pq[i], Q, P);
+    if (pq64) {
+      const double2 v = pq64[i];
+      Q = static_cast<float>(v.x);
+      P = static_cast<float>(v.y);
+    } else {
+      from_fixed(pq[i], fs, Q, P);
+    }
     if (!(fabsf(Q) >= q_floor) && bad) {
       const unsigned long long lin = static_cast<unsigned long long>(b) * g.full_height * g.width +
                                      static_cast<unsigned long long>(g.out_row0 + yl) * g.width + x;
@@ -263,32 +270,89 @@ __global__ void finish_kernel(const p2* __restrict__ pq, float* __restrict__ dst
   }
 }
 
-// ---------------------------------------------------------------------------
-// standalone separable convolution of one fp32 plane (convolve(), spatial.hpp:98-112)
+// Sums the nonempty groups' fixed-point planes (exact integer adds: the
+// result does not depend on the group count) and divides, or writes the exact
+// fp64 (Q, P) values (sum_out, fbf_partial_sums_device).
+// Grid: x = column blocks, y = (image, output row) in a grid-stride loop.
+__global__ void finish_groups(const p2* __restrict__ pq, int groups, int span, long long plane, int pq_cols,
+                              Geometry g, float shift, float q_floor, unsigned long long* bad,
+                              float* __restrict__ dst, double2* __restrict__ sum_out, int aq,
+                              const unsigned* __restrict__ fmax) {
+  const FixedScale fs = fixed_scale(aq, fmax);
+  const long long nrows = static_cast<long long>(g.out_rows) * g.batch;
+  for (long long row = blockIdx.y; row < nrows; row += gridDim.y) {
+    const int b = static_cast<int>(row / g.out_rows);
+    const int yl = static_cast<int>(row - static_cast<long long>(b) * g.out_rows);
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < g.width; x += gridDim.x * blockDim.x) {
+      const long long at = row * pq_cols + x;
+      p2 acc = 0ull;
+      for (int k = 0; k < groups; ++k)
+        if (span * (k + 1) / groups > span * k / groups) acc = iadd2(acc, pq[k * plane + at]);
+      if (sum_out) {  // exact: int32 * 2^-a is representable in fp64
+        float a, c;
+        upk(acc, a, c);
+        sum_out[row * g.width + x] = make_double2(static_cast<double>(__float_as_int(a)) * fs.iq,
+                                                  static_cast<double>(__float_as_int(c)) * fs.ip);
+        continue;
+      }
+      float Q, P;
+      from_fixed(acc, fs, Q, P);
+      if (!(fabsf(Q) >= q_floor) && bad) {
+        const unsigned long long lin = static_cast<unsigned long long>(b) * g.full_height * g.width +
+                                       static_cast<unsigned long long>(g.out_row0 + yl) * g.width + x;
+        atomicMin(bad, lin);
+      }
+      dst[b * g.dst_bstride + static_cast<long long>(yl) * g.dst_pitch + x] = shift + __fdiv_rn(P, Q);
+    }
+  }
+}
+dim3 rows_grid(const Geometry& g) {
+  const long long rows = static_cast<long long>(g.out_rows) * g.batch;
+  return dim3(static_cast<unsigned>((g.width + 255) / 256), static_cast<unsigned>(std::min(rows, 65535LL)), 1);
+}
 
-__global__ void conv_rows_f32(const float* __restrict__ in, float* __restrict__ out, int w, int h,
-                              const __grid_constant__ Taps k) {
+// ---------------------------------------------------------------------------
+// standalone separable convolution of one plane (convolve(), spatial.hpp:98-112):
+// row pass then column pass, out(i) = sum_j profile[j+W] in(i-j) in ascending
+// j.  fp64: separate multiply and add in the reference's order (its build
+// does not contract them), so the result equals the reference bit for bit.
+
+template <class T>
+__device__ __forceinline__ T mac(T t, T v, T acc);
+template <>
+__device__ __forceinline__ float mac<float>(float t, float v, float acc) {
+  return fmaf(t, v, acc);
+}
+template <>
+__device__ __forceinline__ double mac<double>(double t, double v, double acc) {
+  return __dadd_rn(acc, __dmul_rn(t, v));
+}
+
+template <class T>
+__global__ void conv_rows(const T* __restrict__ in, T* __restrict__ out, int w, int h, int W,
+                          const T* __restrict__ taps) {
   const long long total = static_cast<long long>(w) * h;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long rowbase = i - (i % w);
     const int x = static_cast<int>(i % w);
-    float acc = 0.f;
-    for (int j = -k.W; j <= k.W; ++j) acc = fmaf(k.t[j < 0 ? -j : j], in[rowbase + mirror_index(x - j, w)], acc);
+    T acc = 0;
+    for (int j = -W; j <= W; ++j) acc = mac<T>(taps[j + W], in[rowbase + mirror_index(x - j, w)], acc);
     out[i] = acc;
   }
 }
 
-__global__ void conv_cols_f32(const float* __restrict__ in, float* __restrict__ out, int w, int h,
-                              const __grid_constant__ Taps k) {
+template <class T>
+__global__ void conv_cols(const T* __restrict__ in, T* __restrict__ out, int w, int h, int W,
+                          const T* __restrict__ taps) {
   const long long total = static_cast<long long>(w) * h;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int y = static_cast<int>(i / w);
     const int x = static_cast<int>(i % w);
-    float acc = 0.f;
-    for (int j = -k.W; j <= k.W; ++j)
-      acc = fmaf(k.t[j < 0 ? -j : j], in[static_cast<long long>(mirror_index(y - j, h)) * w + x], acc);
+    T acc = 0;
+    for (int j = -W; j <= W; ++j)
+      acc = mac<T>(taps[j + W], in[static_cast<long long>(mirror_index(y - j, h)) * w + x], acc);
     out[i] = acc;
   }
 }
@@ -296,8 +360,7 @@ __global__ void conv_cols_f32(const float* __restrict__ in, float* __restrict__ 
 // ---------------------------------------------------------------------------
 // FP32 FMA-pipe probe: 16 independent FFMA2 chains per thread.
 
-__global__ void __launch_bounds__(256) fma_probe(float* out, float a, float b, int iters,
-                                                 long long* cycles) {
+__global__ void __launch_bounds__(256) fma_probe(float* out, float a, float b, int iters, long long* cycles) {
   p2 acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = pk(threadIdx.x * 1e-3f + i, static_cast<float>(i));
@@ -321,12 +384,14 @@ unsigned grid_for(long long n, int threads) {
   return static_cast<unsigned>(std::max<long long>(g, 1));
 }
 
+// ---------------------------------------------------------------------------
+// host-side checks and parameter blocks
+
 int check_geometry(const fbf_geometry* g) {
   if (!g) return fail(FBF_EINVAL, "bilateral_fast: null geometry");
-  if (g->width <= 0 || g->height <= 0 || g->batch <= 0)
-    return fail(FBF_EINVAL, "bilateral_fast: empty image");
-  if (g->src_row0 < 0 || g->src_rows <= 0 || g->src_row0 + g->src_rows > g->height ||
-      g->out_row0 < 0 || g->out_rows <= 0 || g->out_row0 + g->out_rows > g->height)
+  if (g->width <= 0 || g->height <= 0 || g->batch <= 0) return fail(FBF_EINVAL, "bilateral_fast: empty image");
+  if (g->src_row0 < 0 || g->src_rows <= 0 || g->src_row0 + g->src_rows > g->height || g->out_row0 < 0 ||
+      g->out_rows <= 0 || g->out_row0 + g->out_rows > g->height)
     return fail(FBF_EINVAL, "bilateral_fast: row range outside the image");
   return FBF_OK;
 }
@@ -337,15 +402,26 @@ bool uses_iir(const fbf_filter* f) { return f->kind == FBF_SPATIAL_GAUSSIAN && f
 
 int check_filter(const fbf_filter* f) {
   if (!f || !f->profile || !f->d) return fail(FBF_EINVAL, "bilateral_fast: null filter");
-  if (f->radius < 1 || f->radius > kMaxW)
-    return fail(FBF_EUNSUPPORTED, "bilateral_fast: spatial radius outside [1, 64]");
-  if (f->N < 0 || f->N > kMaxN)
-    return fail(FBF_EUNSUPPORTED, "bilateral_fast: harmonic count outside [0, 65535]");
+  if (f->radius < 1 || f->radius > kMaxRadius)
+    return fail(FBF_EINVAL, "bilateral_fast: spatial radius outside [1, " + std::to_string(kMaxRadius) + "]");
+  if (f->N < 0 || f->N > kMaxN) return fail(FBF_EINVAL, "bilateral_fast: harmonic count outside [0, 65535]");
   if (f->check_epsilon && !(f->max_pointwise_error < f->w0))
     return fail(FBF_EINVAL,
                 "bilateral_fast: kernel approximation error must stay below the center "
                 "spatial weight");
   return FBF_OK;
+}
+
+// The fused kernel keeps one tap per |j| (a symmetric window, as both of
+// make_spatial_gaussian / make_spatial_box produce); any other profile runs the
+// naive chain with the full 2W+1 taps.
+bool symmetric(const fbf_filter* f) {
+  for (int j = 1; j <= f->radius; ++j)
+    if (f->profile[f->radius + j] != f->profile[f->radius - j]) return false;
+  return true;
+}
+bool fused_ok(const fbf_filter* f) {
+  return f->radius <= kMaxWFused && fused_supported(f->radius, f->kind == FBF_SPATIAL_BOX) && symmetric(f);
 }
 
 // The source rows must cover every mirrored row that the output rows touch.
@@ -387,9 +463,19 @@ void fill_taps(Taps& k, const fbf_filter* f) {
   k.W = f->radius;
   k.box = f->kind == FBF_SPATIAL_BOX;
   k.box_tap = static_cast<float>(f->profile[f->radius]);
-  for (int j = 0; j <= f->radius; ++j) {
-    k.t[j] = static_cast<float>(f->profile[f->radius + j]);
-  }
+  for (int j = 0; j <= std::min(f->radius, kMaxWFused); ++j) k.t[j] = static_cast<float>(f->profile[f->radius + j]);
+}
+
+// Q grid exponent of the fixed-point sums (fbf_params.h): the largest aq with
+// 1.02 * D * 2^aq <= 2^31, D = sum over ALL harmonics of |d_n| (as fp32; box
+// windows too: their weight (1/(2W+1))^2 < 1 only shrinks the terms).  A
+// function of the filter alone, so every partition of a call agrees on it.
+int fixed_q_exponent(const fbf_filter* f) {
+  double D = 0.0;
+  for (int n = 0; n <= f->N; ++n) D += std::fabs(static_cast<double>(static_cast<float>(f->d[n])));
+  if (!(D > 0.0)) return 30;
+  const int a = static_cast<int>(std::floor(std::log2(2147483648.0 / (1.02 * D))));
+  return std::max(-60, std::min(40, a));
 }
 
 void fill_harmonics(Harmonics& h, const fbf_filter* f) {
@@ -400,187 +486,96 @@ void fill_harmonics(Harmonics& h, const fbf_filter* f) {
   h.turns_per_unit = f->omega / (2.0 * M_PI);
   h.shift = 128.0f;
   h.q_floor = static_cast<float>((f->w0 - f->max_pointwise_error) / 2.0);
+  h.aq = fixed_q_exponent(f);
 }
 
-struct Layout {
-  size_t uf, pq, m, t, c, total;
-};
-
+// ---------------------------------------------------------------------------
 // Harmonic split inside one GPU: the harmonics are divided among CTA groups,
-// each accumulating its own (Q, P) plane, summed in a fixed order at the end.
-// Each group's CTAs get work units with `groups` times more rows and 1/groups
-// of the harmonics, which cuts the per-harmonic 2W-row unit prologues; large
-// images lose to the extra (Q, P) planes and the finish pass.  The count comes
-// from a cost model (group_model) of the call's own output rows (a rank's
-// strip, a pipeline strip, a whole image) and harmonic count: a strip whose
-// count differs from the whole image's sums its group planes in another order
-// -- equal to fp32 rounding, not bit for bit.
-// Measured: profiles/r01_groups.txt, r01_notes.md.  FBF_GROUPS overrides.
-// the host entry's pipeline strips keep the grouping of the whole call
-// (results independent of the pipeline cut): set around its chunk launches
-thread_local int g_groups_override = 0;
-
-// longest row run a CTA filters per sweep over the harmonics (FBF_SEG_MAX,
-// experiments; default unlimited)
-int seg_max_rows() {
-  static const int v = getenv("FBF_SEG_MAX") ? std::max(16, atoi(getenv("FBF_SEG_MAX"))) : (1 << 30);
-  return v;
-}
-
-int forced_groups() {
-  static const int forced = [] {
-    const char* e = getenv("FBF_GROUPS");
-    return e ? std::max(1, std::min(8, atoi(e))) : 0;
-  }();
-  return forced;
-}
+// each accumulating its own fixed-point (Q, P) plane, summed exactly at the
+// end.  Each group's CTAs get work units with `groups` times more rows and
+// 1/groups of the harmonics, which cuts the per-harmonic 2W-row unit
+// prologues; large images lose to the extra planes and the finish pass.  The
+// count comes from a cost model (group_model) of the call's own output rows
+// and harmonic count.  Since the sums are integers, any count gives the same
+// bits.  Measured: profiles/r01_groups.txt, r01_notes.md.
 
 // Cost model, in CTA rows of one harmonic: a CTA of group count k filters
 // ceil(H / k) harmonics over R / floor(ctas / k) rows, each harmonic paying
 // its unit's prologue (~0.55 * 2W rows, the fused kernel's unit cost).  A
-// larger k must win by 3 %: the extra (Q, P) planes and the finish pass are
-// not in the model (measured: c1 13 harmonics -> 7 groups, c3 31 -> 4,
-// c2 21 -> 1; profiles/r01_notes.md).
+// larger k must win by 3 %: the extra planes and the finish pass are not in
+// the model (measured: c1 13 harmonics -> 7 groups, c3 31 -> 4, c2 21 -> 1).
 int group_model(const fbf_geometry* g, int radius, int H) {
-  static const int sms = [] {
-    int dev = 0, n = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n > 0 ? n : 148;
-  }();
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) sm_count(dev, &sms);
   const int ctas = sms * (radius <= 9 ? 2 : 1);  // launch_w: small CTAs for W <= 9
   const double strips = std::ceil(g->width / static_cast<double>(kFusedTW));
   const double rows = static_cast<double>(g->out_rows) * g->batch * strips;
-  const double u = 2.0 * radius * 0.55;
+  const double u = 2.0 * radius * FBF_TUNABLE(UNIT_COST_FRAC, kUnitCostFrac);
+  const double margin = FBF_TUNABLE(GROUP_MARGIN, kGroupMargin);
   auto cost = [&](int k) { return ((H + k - 1) / k) * (rows / (ctas / k) + u); };
   int groups = 1;
   double best = cost(1);
   for (int k = 2; k <= std::min({8, H, ctas}); ++k) {
     const double c = cost(k);
-    if (c < 0.97 * best) best = c, groups = k;
+    if (c < margin * best) best = c, groups = k;
   }
+#ifdef FBF_EXPERIMENTS
+  if (const char* e = getenv("FBF_GROUPS")) groups = std::max(1, std::min(8, atoi(e)));
+#endif
   return groups;
 }
 
 // (Q, P) planes the workspace holds for this geometry: the most any harmonic
-// count (per launch: <= kMaxD) picks
+// count (per launch: <= kMaxD) picks (memoised per thread: the host entry asks
+// several times per call)
 int group_cap(const fbf_geometry* g, int radius) {
-  if (g_groups_override) return g_groups_override;
-  if (forced_groups()) return forced_groups();
-  // a few hundred model evaluations: memoised per thread (the host entry asks
-  // several times per call)
   struct Memo {
-    int out_rows = -1, width = -1, batch = -1, radius = -1, cap = 1;
+    int out_rows = -1, width = -1, batch = -1, radius = -1, dev = -1, cap = 1;
   };
   thread_local Memo m;
-  if (m.out_rows == g->out_rows && m.width == g->width && m.batch == g->batch && m.radius == radius) return m.cap;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (m.out_rows == g->out_rows && m.width == g->width && m.batch == g->batch && m.radius == radius && m.dev == dev)
+    return m.cap;
   int cap = 1;
   for (int H = 2; H <= kMaxD && cap < 8; ++H) cap = std::max(cap, group_model(g, radius, H));
-  m = Memo{g->out_rows, g->width, g->batch, radius, cap};
+  m = Memo{g->out_rows, g->width, g->batch, radius, dev, cap};
   return cap;
 }
 
 int harmonic_groups(const fbf_geometry* g, int radius, int harmonics) {
-  if (g_groups_override) return g_groups_override;
-  if (forced_groups()) return forced_groups();
   return std::min(group_model(g, radius, std::min(harmonics, kMaxD)), group_cap(g, radius));
 }
 
-// sum of the nonempty groups' (Q, P) planes -> divide (or -> a dense plane)
-// grid (column blocks, output rows, images): one block row per output row
-__global__ void finish_groups(const p2* __restrict__ pq, int groups, int span, long long plane, int pq_cols,
-                              Geometry g, float shift, float q_floor, unsigned long long* bad,
-                              float* __restrict__ dst, p2* __restrict__ sum_out) {
-  const int yl = blockIdx.y, b = blockIdx.z;
-  const long long row = (static_cast<long long>(b) * g.out_rows + yl);
-  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < g.width; x += gridDim.x * blockDim.x) {
-    const long long at = row * pq_cols + x;
-    p2 acc = 0ull;
-    for (int k = 0; k < groups; ++k)  // fixed order: deterministic
-      if (span * (k + 1) / groups > span * k / groups) acc = add2(acc, pq[k * plane + at]);
-    if (sum_out) {
-      sum_out[row * g.width + x] = acc;
-      continue;
-    }
-    float Q, P;
-    upk(acc, Q, P);
-    if (!(fabsf(Q) >= q_floor) && bad) {
-      const unsigned long long lin = static_cast<unsigned long long>(b) * g.full_height * g.width +
-                                     static_cast<unsigned long long>(g.out_row0 + yl) * g.width + x;
-      atomicMin(bad, lin);
-    }
-    dst[b * g.dst_bstride + static_cast<long long>(yl) * g.dst_pitch + x] = shift + __fdiv_rn(P, Q);
-  }
-}
-dim3 rows_grid(const Geometry& g) {
-  return dim3(static_cast<unsigned>((g.width + 255) / 256), static_cast<unsigned>(g.out_rows),
-              static_cast<unsigned>(g.batch));
-}
+struct Layout {
+  size_t hdr, uf, pq, taps, m, t, c, total;  // hdr: 256-byte header, word 0 = max |f'| bits (prep)
+};
 
-// Fused: mirror-padded (u, f') image (out_rows + 2W) x (strips*TW + 2W) and a
-// (Q, P) plane out_rows x strips*TW per image (see FusedArgs).  Naive: dense
-// (u, f') of the source rows, (Q, P) per output pixel and three float4 planes.
+// Fused: mirror-padded (u, f') image (out_rows + 2W) x (strips*TW + 2W) and
+// group_cap fixed-point (Q, P) planes out_rows x strips*TW per image.  Naive:
+// dense (u, f') of the source rows, (Q, P) per output pixel, the taps and
+// three float4 planes.
 Layout layout_of(const fbf_geometry* g, int radius, int variant) {
   Layout L{};
   const size_t src_px = static_cast<size_t>(g->batch) * g->src_rows * g->width;
   const size_t out_px = static_cast<size_t>(g->batch) * g->out_rows * g->width;
-  L.uf = 0;
+  L.hdr = 0;
+  L.uf = 256;
   if (variant == FBF_VARIANT_FUSED) {
     const size_t cols = static_cast<size_t>((g->width + kFusedTW - 1) / kFusedTW) * kFusedTW;
     const size_t uf_px = static_cast<size_t>(g->batch) * (g->out_rows + 2 * radius) * (cols + 2 * radius);
-    L.pq = align256(uf_px * sizeof(int2));
-    L.total = L.pq + align256(static_cast<size_t>(group_cap(g, radius)) * g->batch * g->out_rows * cols *
-                              sizeof(Pair));
+    L.pq = L.uf + align256(uf_px * sizeof(int2));
+    L.total = L.pq + align256(static_cast<size_t>(group_cap(g, radius)) * g->batch * g->out_rows * cols * sizeof(Pair));
     return L;
   }
-  L.pq = align256(src_px * sizeof(int2));
-  size_t end = L.pq + align256(out_px * sizeof(Pair));
-  {
-    L.m = end;
-    L.t = L.m + align256(src_px * sizeof(float4));
-    L.c = L.t + align256(src_px * sizeof(float4));
-    end = L.c + align256(out_px * sizeof(float4));
-  }
-  L.total = end;
+  L.pq = L.uf + align256(src_px * sizeof(int2));
+  L.taps = L.pq + align256(out_px * sizeof(Pair));
+  L.m = L.taps + align256((2 * static_cast<size_t>(radius) + 1) * sizeof(float));
+  L.t = L.m + align256(src_px * sizeof(float4));
+  L.c = L.t + align256(src_px * sizeof(float4));
+  L.total = L.c + align256(out_px * sizeof(float4));
   return L;
 }
-
-}  // namespace
-
-extern "C" {
-
-const char* fbf_last_error(void) { return g_err.c_str(); }
-int fbf_version(void) { return 1; }
-
-void fbf_geometry_whole(fbf_geometry* g, int width, int height, int batch) {
-  g->width = width;
-  g->height = height;
-  g->batch = batch;
-  g->src_row0 = 0;
-  g->src_rows = height;
-  g->out_row0 = 0;
-  g->out_rows = height;
-  g->src_pitch = width;
-  g->dst_pitch = width;
-  g->src_bstride = static_cast<long long>(width) * height;
-  g->dst_bstride = static_cast<long long>(width) * height;
-}
-
-size_t fbf_workspace_bytes(const fbf_geometry* g, int radius, int variant) {
-  if (check_geometry(g) != FBF_OK || radius < 1 || radius > kMaxW) return 0;
-  if (variant == FBF_VARIANT_RECURSIVE)  // the IIR path, or the direct path it falls back to
-    return std::max(iir_workspace_bytes(g, radius), fbf_workspace_bytes(g, radius, FBF_VARIANT_FUSED));
-  if (variant == FBF_VARIANT_FUSED) {
-    const bool g_ok = fused_supported(radius, false), b_ok = fused_supported(radius, true);
-    if (!g_ok && !b_ok) variant = FBF_VARIANT_NAIVE;
-    // the window kind is not known here: cover both paths when they differ
-    if (g_ok != b_ok)
-      return std::max(layout_of(g, radius, FBF_VARIANT_FUSED).total,
-                      layout_of(g, radius, FBF_VARIANT_NAIVE).total);
-  }
-  return layout_of(g, radius, variant).total;
-}
-
-namespace {
 
 struct Prepared {
   Geometry G, Gd;
@@ -589,9 +584,43 @@ struct Prepared {
   int variant;
   int2* uf;
   Pair* pq;
+  unsigned* fmax;
   char* ws;
   Layout L;
 };
+
+int prepare_common(const fbf_geometry* gp, const fbf_filter* f, void* workspace, size_t workspace_bytes, int variant,
+                   Prepared& P) {
+  int rc = check_geometry(gp);
+  if (rc) return rc;
+  if ((rc = check_filter(f))) return rc;
+  if ((rc = check_halo(gp, f->radius))) return rc;
+  if (variant == FBF_VARIANT_RECURSIVE) {
+    if (uses_iir(f))
+      return fail(FBF_EUNSUPPORTED,
+                  "bilateral_fast: the recursive backend runs through fbf_bilateral_fast_device / _host only");
+    variant = FBF_VARIANT_FUSED;  // spatial.hpp:102-104: box windows and sigma < 2 stay direct
+  }
+  if (variant == FBF_VARIANT_FUSED && !fused_ok(f)) variant = FBF_VARIANT_NAIVE;
+  P.L = layout_of(gp, f->radius, variant);
+  if (!workspace || workspace_bytes < P.L.total)
+    return fail(FBF_EINVAL, variant == FBF_VARIANT_NAIVE
+                                ? "bilateral_fast: workspace too small for the naive path (no fused "
+                                  "kernel for this window)"
+                                : "bilateral_fast: workspace too small");
+  P.variant = variant;
+  P.ws = static_cast<char*>(workspace);
+  P.fmax = reinterpret_cast<unsigned*>(P.ws + P.L.hdr);
+  P.uf = reinterpret_cast<int2*>(P.ws + P.L.uf);
+  P.pq = reinterpret_cast<Pair*>(P.ws + P.L.pq);
+  P.G = to_geometry(gp);
+  fill_harmonics(P.H, f);
+  fill_taps(P.K, f);
+  P.Gd = P.G;  // dense view of the prep output: batch x src_rows x width
+  P.Gd.src_pitch = P.G.width;
+  P.Gd.src_bstride = static_cast<long long>(P.G.src_rows) * P.G.width;
+  return FBF_OK;
+}
 
 // Fused launches over harmonics [n_lo, n_hi): one launch when the range fits
 // the kMaxD coefficients of a parameter block (the common case, N < 256),
@@ -617,117 +646,177 @@ int launch_fused_range(const FusedArgs& base, const fbf_filter* f, int n_lo, int
   return A.groups;
 }
 
-int prepare_common(const fbf_geometry* gp, const fbf_filter* f, void* workspace,
-                   size_t workspace_bytes, int variant, Prepared& P) {
-  int rc = check_geometry(gp);
-  if (rc) return rc;
-  if ((rc = check_filter(f))) return rc;
-  if ((rc = check_halo(gp, f->radius))) return rc;
-  if (variant == FBF_VARIANT_RECURSIVE) {
-    if (uses_iir(f))
-      return fail(FBF_EUNSUPPORTED,
-                  "bilateral_fast: the recursive backend runs through fbf_bilateral_fast_device / _host only");
-    variant = FBF_VARIANT_FUSED;  // spatial.hpp:102-104: box windows and sigma < 2 stay direct
-  }
-  if (variant == FBF_VARIANT_FUSED && !fused_supported(f->radius, f->kind == FBF_SPATIAL_BOX)) variant = FBF_VARIANT_NAIVE;
-  P.L = layout_of(gp, f->radius, variant);
-  if (!workspace || workspace_bytes < P.L.total)
-    return fail(FBF_EINVAL, variant == FBF_VARIANT_NAIVE
-                                ? "bilateral_fast: workspace too small for the naive path (no fused "
-                                  "kernel is compiled for this radius)"
-                                : "bilateral_fast: workspace too small");
-  P.variant = variant;
-  P.ws = static_cast<char*>(workspace);
-  P.uf = reinterpret_cast<int2*>(P.ws + P.L.uf);
-  P.pq = reinterpret_cast<Pair*>(P.ws + P.L.pq);
-  P.G = to_geometry(gp);
-  fill_harmonics(P.H, f);
-  fill_taps(P.K, f);
-  P.Gd = P.G;  // dense view of the prep output: batch x src_rows x width
-  P.Gd.src_pitch = P.G.width;
-  P.Gd.src_bstride = static_cast<long long>(P.G.src_rows) * P.G.width;
-  return FBF_OK;
+FusedArgs fused_args(const Prepared& P, float* dst, unsigned long long* d_bad) {
+  FusedArgs A;
+  std::memset(&A, 0, sizeof(A));
+  A.g = P.Gd;
+  A.h = P.H;
+  A.k = P.K;
+  A.uf = P.uf;
+  A.dst = dst;
+  A.pq = P.pq;
+  A.fmax = P.fmax;
+  A.bad = d_bad;
+  A.seg_max = 1 << 30;
+  return A;
 }
 
-}  // namespace
-
-int fbf_prepare_device(const fbf_geometry* gp, const fbf_filter* f, const float* src,
-                       void* workspace, size_t workspace_bytes, int variant, void* stream) {
-  Prepared P;
-  int rc = prepare_common(gp, f, workspace, workspace_bytes, variant, P);
-  if (rc) return rc;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const double scale = P.H.turns_per_unit * 4294967296.0;
-  if (P.variant == FBF_VARIANT_FUSED) {
-    const int W = f->radius;
-    const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
-    const int pairs = (cols + 2 * W) / 2;  // cols is a multiple of 64: even row length
-    const dim3 grid((pairs + 127) / 128, P.G.out_rows + 2 * W, P.G.batch);
-    prep_padded_kernel<<<grid, 128, 0, st>>>(src, P.uf, P.G, W, cols, scale, P.H.shift);
-  } else {
-    const long long src_px = static_cast<long long>(P.G.batch) * P.G.src_rows * P.G.width;
-    prep_kernel<<<grid_for(src_px, 256), 256, 0, st>>>(src, P.uf, P.G, scale, P.H.shift);
-  }
-  FBF_CUDA(cudaGetLastError());
-  return FBF_OK;
-}
-
-int fbf_filter_prepared_device(const fbf_geometry* gp, const fbf_filter* f, float* dst,
-                               void* workspace, size_t workspace_bytes, unsigned long long* d_bad,
-                               int variant, void* stream) {
-  Prepared P;
-  int rc = prepare_common(gp, f, workspace, workspace_bytes, variant, P);
-  if (rc) return rc;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (P.variant == FBF_VARIANT_FUSED) {
-    FusedArgs A;
-    std::memset(&A, 0, sizeof(A));
-    A.g = P.Gd;
-    A.h = P.H;
-    A.k = P.K;
-    A.uf = P.uf;
-    A.dst = dst;
-    A.pq = P.pq;
-    A.bad = d_bad;
-    A.seg_max = seg_max_rows();
-    cudaError_t e = cudaSuccess;
-    const int groups = launch_fused_range(A, f, 0, P.H.N + 1, harmonic_groups(gp, f->radius, P.H.N + 1), false, st, &e);
-    FBF_CUDA(e);
-    if (groups > 1) {
-      const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
-      const long long plane = static_cast<long long>(P.G.batch) * P.G.out_rows * cols;
-      const long long out_px = static_cast<long long>(P.G.batch) * P.G.out_rows * P.G.width;
-      finish_groups<<<rows_grid(P.G), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), groups, P.H.N + 1,
-                                                    plane, cols, P.G, P.H.shift, P.H.q_floor, d_bad, dst,
-                                                    nullptr);
-      FBF_CUDA(cudaGetLastError());
-    }
-    return FBF_OK;
-  }
-  // naive: HBM-resident planes, four kernels per harmonic
+// the naive chain over harmonics [n_lo, n_hi) into the fixed-point (Q, P) plane
+int naive_range(const Prepared& P, const fbf_filter* f, int n_lo, int n_hi, cudaStream_t st) {
   ulonglong2* M = reinterpret_cast<ulonglong2*>(P.ws + P.L.m);
   ulonglong2* T = reinterpret_cast<ulonglong2*>(P.ws + P.L.t);
   ulonglong2* C = reinterpret_cast<ulonglong2*>(P.ws + P.L.c);
   NaiveArgs NA;
   NA.g = P.Gd;
-  NA.k = P.K;
+  NA.W = f->radius;
+  NA.taps = reinterpret_cast<const float*>(P.ws + P.L.taps);
   const long long src_px = static_cast<long long>(P.G.batch) * P.G.src_rows * P.G.width;
   const long long out_px = static_cast<long long>(P.G.batch) * P.G.out_rows * P.G.width;
-  for (int n = 0; n <= P.H.N; ++n) {
+  for (int n = n_lo; n < n_hi; ++n) {
     naive_modulate<<<grid_for(src_px, 256), 256, 0, st>>>(P.uf, M, src_px, static_cast<uint32_t>(n));
     naive_rows<<<grid_for(src_px, 256), 256, 0, st>>>(M, T, NA);
     naive_cols<<<grid_for(out_px, 256), 256, 0, st>>>(T, C, NA);
     naive_demod<<<grid_for(out_px, 256), 256, 0, st>>>(M, C, reinterpret_cast<p2*>(P.pq), P.Gd,
-                                                       static_cast<float>(f->d[n]), n == 0);
+                                                       static_cast<float>(f->d[n]), n == n_lo, P.H.aq, P.fmax);
   }
-  finish_kernel<<<grid_for(out_px, 256), 256, 0, st>>>(reinterpret_cast<p2*>(P.pq), dst, P.G, P.H.shift, P.H.q_floor, d_bad);
   FBF_CUDA(cudaGetLastError());
   return FBF_OK;
 }
 
-int fbf_bilateral_fast_device(const fbf_geometry* gp, const fbf_filter* f, const float* src,
-                              float* dst, void* workspace, size_t workspace_bytes,
-                              unsigned long long* d_bad, int variant, void* stream) {
+template <class T>
+int convolve_any(int width, int height, const double* profile, int radius, const T* src, T* dst, void* workspace,
+                 size_t workspace_bytes, cudaStream_t st) {
+  if (width <= 0 || height <= 0) return fail(FBF_EINVAL, "convolve: empty plane");
+  if (radius < 0 || radius > kMaxRadius || !profile) return fail(FBF_EINVAL, "convolve: invalid spatial kernel");
+  const size_t n = static_cast<size_t>(width) * height;
+  const size_t need = align256(n * sizeof(T)) + align256((2 * static_cast<size_t>(radius) + 1) * sizeof(T));
+  if (!workspace || workspace_bytes < need) return fail(FBF_EINVAL, "convolve: workspace too small");
+  T* tmp = static_cast<T*>(workspace);
+  T* taps = reinterpret_cast<T*>(static_cast<char*>(workspace) + align256(n * sizeof(T)));
+  if constexpr (sizeof(T) == 4) {
+    FBF_CUDA(upload_taps(profile, radius, reinterpret_cast<float*>(taps), nullptr, st));
+  } else {
+    FBF_CUDA(upload_taps(profile, radius, nullptr, reinterpret_cast<double*>(taps), st));
+  }
+  conv_rows<T><<<grid_for(n, 256), 256, 0, st>>>(src, tmp, width, height, radius, taps);
+  conv_cols<T><<<grid_for(n, 256), 256, 0, st>>>(tmp, dst, width, height, radius, taps);
+  FBF_CUDA(cudaGetLastError());
+  return FBF_OK;
+}
+
+}  // namespace
+
+namespace fbf {
+// internal API for the host path (fbf_hostpath.cu)
+size_t workspace_for(const fbf_geometry* g, const fbf_filter* f, int variant) {
+  if (variant == FBF_VARIANT_RECURSIVE) {
+    if (uses_iir(f)) return iir_workspace_bytes(g, f->radius);
+    variant = FBF_VARIANT_FUSED;
+  }
+  if (variant == FBF_VARIANT_FUSED && !fused_ok(f)) variant = FBF_VARIANT_NAIVE;
+  return layout_of(g, f->radius, variant).total;
+}
+int check_call(const fbf_geometry* g, const fbf_filter* f) {
+  int rc = check_geometry(g);
+  if (rc == FBF_OK) rc = check_filter(f);
+  if (rc == FBF_OK) rc = check_halo(g, f->radius);
+  return rc;
+}
+bool recursive_applies(const fbf_filter* f) { return uses_iir(f); }
+bool fused_applies(const fbf_filter* f) { return fused_ok(f); }
+}  // namespace fbf
+
+extern "C" {
+
+const char* fbf_last_error(void) { return g_err.c_str(); }
+int fbf_version(void) { return 2; }
+
+void fbf_geometry_whole(fbf_geometry* g, int width, int height, int batch) {
+  g->width = width;
+  g->height = height;
+  g->batch = batch;
+  g->src_row0 = 0;
+  g->src_rows = height;
+  g->out_row0 = 0;
+  g->out_rows = height;
+  g->src_pitch = width;
+  g->dst_pitch = width;
+  g->src_bstride = static_cast<long long>(width) * height;
+  g->dst_bstride = static_cast<long long>(width) * height;
+}
+
+size_t fbf_workspace_bytes(const fbf_geometry* g, int radius, int variant) {
+  if (check_geometry(g) != FBF_OK || radius < 1 || radius > kMaxRadius) return 0;
+  if (variant == FBF_VARIANT_RECURSIVE)  // the IIR path, or the direct path it falls back to
+    return std::max(iir_workspace_bytes(g, radius), fbf_workspace_bytes(g, radius, FBF_VARIANT_FUSED));
+  if (variant == FBF_VARIANT_FUSED) {
+    const bool g_ok = radius <= kMaxWFused && fused_supported(radius, false);
+    const bool b_ok = radius <= kMaxWFused && fused_supported(radius, true);
+    if (!g_ok && !b_ok) variant = FBF_VARIANT_NAIVE;
+    // the window kind is not known here: cover both paths when they differ
+    if (g_ok != b_ok)
+      return std::max(layout_of(g, radius, FBF_VARIANT_FUSED).total, layout_of(g, radius, FBF_VARIANT_NAIVE).total);
+  }
+  return layout_of(g, radius, variant).total;
+}
+
+int fbf_prepare_device(const fbf_geometry* gp, const fbf_filter* f, const float* src, void* workspace,
+                       size_t workspace_bytes, int variant, void* stream) {
+  Prepared P;
+  int rc = prepare_common(gp, f, workspace, workspace_bytes, variant, P);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const double scale = P.H.turns_per_unit * 4294967296.0;
+  FBF_CUDA(cudaMemsetAsync(P.fmax, 0, sizeof(unsigned), st));
+  if (P.variant == FBF_VARIANT_FUSED) {
+    const int W = f->radius;
+    const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
+    const int pairs = (cols + 2 * W) / 2;  // cols is a multiple of 64: even row length
+    const long long rows = static_cast<long long>(P.G.out_rows + 2 * W) * P.G.batch;
+    const dim3 grid((pairs + 127) / 128, static_cast<unsigned>(std::min(rows, 65535LL)), 1);
+    prep_padded_kernel<<<grid, 128, 0, st>>>(src, P.uf, P.G, W, cols, scale, P.H.shift, P.fmax);
+  } else {
+    const long long src_px = static_cast<long long>(P.G.batch) * P.G.src_rows * P.G.width;
+    prep_kernel<<<grid_for(src_px, 256), 256, 0, st>>>(src, P.uf, P.G, scale, P.H.shift, P.fmax);
+    FBF_CUDA(upload_taps(f->profile, f->radius, reinterpret_cast<float*>(P.ws + P.L.taps), nullptr, st));
+  }
+  FBF_CUDA(cudaGetLastError());
+  return FBF_OK;
+}
+
+int fbf_filter_prepared_device(const fbf_geometry* gp, const fbf_filter* f, float* dst, void* workspace,
+                               size_t workspace_bytes, unsigned long long* d_bad, int variant, void* stream) {
+  Prepared P;
+  int rc = prepare_common(gp, f, workspace, workspace_bytes, variant, P);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (P.variant == FBF_VARIANT_FUSED) {
+    const FusedArgs A = fused_args(P, dst, d_bad);
+    cudaError_t e = cudaSuccess;
+    const int groups =
+        launch_fused_range(A, f, 0, P.H.N + 1, harmonic_groups(gp, f->radius, P.H.N + 1), false, st, &e);
+    FBF_CUDA(e);
+    if (groups > 1) {
+      const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
+      const long long plane = static_cast<long long>(P.G.batch) * P.G.out_rows * cols;
+      finish_groups<<<rows_grid(P.G), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), groups, P.H.N + 1, plane,
+                                                    cols, P.G, P.H.shift, P.H.q_floor, d_bad, dst, nullptr, P.H.aq,
+                                                    P.fmax);
+      FBF_CUDA(cudaGetLastError());
+    }
+    return FBF_OK;
+  }
+  if ((rc = naive_range(P, f, 0, P.H.N + 1, st))) return rc;
+  const long long out_px = static_cast<long long>(P.G.batch) * P.G.out_rows * P.G.width;
+  finish_kernel<<<grid_for(out_px, 256), 256, 0, st>>>(reinterpret_cast<p2*>(P.pq), nullptr, dst, P.G, P.H.shift,
+                                                       P.H.q_floor, d_bad, P.H.aq, P.fmax);
+  FBF_CUDA(cudaGetLastError());
+  return FBF_OK;
+}
+
+int fbf_bilateral_fast_device(const fbf_geometry* gp, const fbf_filter* f, const float* src, float* dst,
+                              void* workspace, size_t workspace_bytes, unsigned long long* d_bad, int variant,
+                              void* stream) {
   if (variant == FBF_VARIANT_RECURSIVE) {
     int rc = check_geometry(gp);
     if (rc) return rc;
@@ -742,7 +831,7 @@ int fbf_bilateral_fast_device(const fbf_geometry* gp, const fbf_filter* f, const
   return fbf_filter_prepared_device(gp, f, dst, workspace, workspace_bytes, d_bad, variant, stream);
 }
 
-int fbf_partial_sums_device(const fbf_geometry* gp, const fbf_filter* f, int n_lo, int n_hi, float* pq_out,
+int fbf_partial_sums_device(const fbf_geometry* gp, const fbf_filter* f, int n_lo, int n_hi, double* pq_out,
                             void* workspace, size_t workspace_bytes, int variant, void* stream) {
   Prepared P;
   int rc = prepare_common(gp, f, workspace, workspace_bytes, variant, P);
@@ -750,46 +839,28 @@ int fbf_partial_sums_device(const fbf_geometry* gp, const fbf_filter* f, int n_l
   if (n_lo < 0 || n_hi > P.H.N + 1 || n_lo >= n_hi || !pq_out)
     return fail(FBF_EINVAL, "partial_sums: harmonic range outside [0, N]");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const long long out_px = static_cast<long long>(P.G.batch) * P.G.out_rows * P.G.width;
+  int groups = 1, span = n_hi - n_lo;
+  long long plane = 0;
+  int cols = P.G.width;
   if (P.variant == FBF_VARIANT_FUSED) {
-    FusedArgs A;
-    std::memset(&A, 0, sizeof(A));
-    A.g = P.Gd;
-    A.h = P.H;
-    A.k = P.K;
-    A.uf = P.uf;
-    A.pq = P.pq;
-    A.seg_max = seg_max_rows();
+    const FusedArgs A = fused_args(P, nullptr, nullptr);
     cudaError_t e = cudaSuccess;
-    const int groups = launch_fused_range(A, f, n_lo, n_hi, harmonic_groups(gp, f->radius, n_hi - n_lo), true, st, &e);
+    groups = launch_fused_range(A, f, n_lo, n_hi, harmonic_groups(gp, f->radius, n_hi - n_lo), true, st, &e);
     FBF_CUDA(e);
-    const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
-    const long long plane = static_cast<long long>(P.G.batch) * P.G.out_rows * cols;
-    finish_groups<<<rows_grid(P.G), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), groups, n_hi - n_lo,
-                                                  plane, cols, P.G, 0.f, 0.f, nullptr, nullptr,
-                                                  reinterpret_cast<p2*>(pq_out));
-    FBF_CUDA(cudaGetLastError());
-    return FBF_OK;
+    cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
+    plane = static_cast<long long>(P.G.batch) * P.G.out_rows * cols;
+  } else {
+    if ((rc = naive_range(P, f, n_lo, n_hi, st))) return rc;
+    span = 1;
   }
-  ulonglong2* M = reinterpret_cast<ulonglong2*>(P.ws + P.L.m);
-  ulonglong2* T = reinterpret_cast<ulonglong2*>(P.ws + P.L.t);
-  ulonglong2* Cc = reinterpret_cast<ulonglong2*>(P.ws + P.L.c);
-  NaiveArgs NA;
-  NA.g = P.Gd;
-  NA.k = P.K;
-  const long long src_px = static_cast<long long>(P.G.batch) * P.G.src_rows * P.G.width;
-  for (int n = n_lo; n < n_hi; ++n) {
-    naive_modulate<<<grid_for(src_px, 256), 256, 0, st>>>(P.uf, M, src_px, static_cast<uint32_t>(n));
-    naive_rows<<<grid_for(src_px, 256), 256, 0, st>>>(M, T, NA);
-    naive_cols<<<grid_for(out_px, 256), 256, 0, st>>>(T, Cc, NA);
-    naive_demod<<<grid_for(out_px, 256), 256, 0, st>>>(M, Cc, reinterpret_cast<p2*>(pq_out), P.Gd,
-                                                       static_cast<float>(f->d[n]), n == n_lo);
-  }
+  finish_groups<<<rows_grid(P.G), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), groups, span, plane, cols, P.G,
+                                                0.f, 0.f, nullptr, nullptr, reinterpret_cast<double2*>(pq_out), P.H.aq,
+                                                P.fmax);
   FBF_CUDA(cudaGetLastError());
   return FBF_OK;
 }
 
-int fbf_finish_device(const fbf_geometry* gp, const fbf_filter* f, const float* pq, float* dst,
+int fbf_finish_device(const fbf_geometry* gp, const fbf_filter* f, const double* pq, float* dst,
                       unsigned long long* d_bad, void* stream) {
   int rc = check_geometry(gp);
   if (rc) return rc;
@@ -799,7 +870,7 @@ int fbf_finish_device(const fbf_geometry* gp, const fbf_filter* f, const float* 
   const Geometry G = to_geometry(gp);
   const long long out_px = static_cast<long long>(G.batch) * G.out_rows * G.width;
   finish_kernel<<<grid_for(out_px, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const p2*>(pq), dst, G, H.shift, H.q_floor, d_bad);
+      nullptr, reinterpret_cast<const double2*>(pq), dst, G, H.shift, H.q_floor, d_bad, H.aq, nullptr);
   FBF_CUDA(cudaGetLastError());
   return FBF_OK;
 }
@@ -815,450 +886,31 @@ int fbf_launches_per_call(const fbf_geometry* g, const fbf_filter* f, int varian
     if (uses_iir(f)) return g->batch * (6 * (f->N + 1) + 1);  // per harmonic: modulate, 2 IIR, 2 transposes, demod
     variant = FBF_VARIANT_FUSED;
   }
-  if (variant == FBF_VARIANT_FUSED && fused_supported(f->radius, f->kind == FBF_SPATIAL_BOX)) {
+  if (variant == FBF_VARIANT_FUSED && fused_ok(f)) {
     const int chunks = (f->N + kMaxD) / kMaxD;  // fused launches of <= kMaxD harmonics
     if (chunks > 1) return 1 + chunks;
     return std::min(harmonic_groups(g, f->radius, f->N + 1), f->N + 1) > 1 ? 3 : 2;  // prep, fused (, group sum)
   }
-  return 1 + 4 * (f->N + 1) + 1;
+  const int tap_uploads = (2 * f->radius + 1 + kTapChunk - 1) / kTapChunk;
+  return 1 + tap_uploads + 4 * (f->N + 1) + 1;
 }
 
-// Host-buffer entry point, pipelined: the work is cut into K chunks (whole
-// images of a batch, or row strips of one large image) issued alternately on
-// two streams, so chunk k's H2D / D2H copies overlap the kernels of its
-// neighbours.  Row strips carry their W halo rows (mirror only at the global
-// edges) and are cut on multiples of 16 rows.  A strip run with the whole
-// call's harmonic grouping reproduces one launch bit for bit; with its own
-// grouping (the default, see below) it agrees to fp32 rounding of the group
-// sums (tests/test_gpu_device.py).
-// Batches: up to 8 image chunks.  One image: K strips from a measured cost
-// model (plan_chunks).
-namespace {
-
-struct Chunk {
-  int b0, nb;     // images [b0, b0 + nb)
-  int o0, o1;     // output rows (global) [o0, o1)
-  int s0, s1;     // source rows (global) [s0, s1) held on the device for this chunk
-};
-
-// calls below this many pixels run as one launch (CUDA-graph replayed); from
-// 1 Mpixel on, two strips already hide half the copies (c3 1024^2 e2e
-// 0.404 -> 0.36 ms, tools/e2e_probe.py); FBF_HOST_MIN_MPX overrides (experiments)
-double pipeline_min_px() {
-  static const double v = getenv("FBF_HOST_MIN_MPX") ? atof(getenv("FBF_HOST_MIN_MPX")) * 1e6 : 1.0e6;
-  return v;
+size_t fbf_convolve_workspace_bytes(int width, int height, int radius) {
+  if (width <= 0 || height <= 0 || radius < 0) return 0;
+  return align256(static_cast<size_t>(width) * height * sizeof(double)) +
+         align256((2 * static_cast<size_t>(radius) + 1) * sizeof(double));
 }
 
-std::vector<Chunk> plan_chunks(const fbf_geometry* g, int W, int variant) {
-  std::vector<Chunk> c;
-  const double px = static_cast<double>(g->width) * g->out_rows * g->batch;
-  if (variant != FBF_VARIANT_FUSED || px < pipeline_min_px()) {  // small: one launch
-    c.push_back({0, g->batch, g->out_row0, g->out_row0 + g->out_rows, g->src_row0, g->src_row0 + g->src_rows});
-    return c;
-  }
-  if (g->batch >= 2) {  // whole images per chunk (up to 16: c5 e2e 5320 -> 5529 against 8); first and last chunk at 20 % weight
-    static const int kmax = getenv("FBF_HOST_BATCH_CHUNKS") ? std::max(2, atoi(getenv("FBF_HOST_BATCH_CHUNKS"))) : 16;
-    const int k = std::min(g->batch, std::min(kmax, 16));  // 16: the pipeline's chunk limit
-    const long long e = k >= 3 ? 20 : 100, wsum = 2 * e + 100LL * (k - 2);
-    auto cut = [&](int i) {
-      const long long w = i == 0 ? 0 : i == k ? wsum : e + 100LL * (i - 1);
-      return static_cast<int>(g->batch * w / wsum);
-    };
-    for (int i = 0; i < k; ++i) {
-      const int b0 = cut(i), b1 = cut(i + 1);
-      if (b1 > b0)
-        c.push_back({b0, b1 - b0, g->out_row0, g->out_row0 + g->out_rows, g->src_row0, g->src_row0 + g->src_rows});
-    }
-    return c;
-  }
-  // one image: K strips cost ~ a + b/K + c*K (b: the copies a strip pipeline
-  // hides, c: per-strip prologue rows, launch and tail); fitted on c2 / c4
-  // (profiles/r01_notes.md): K ~ sqrt(b/c) ~ sqrt(pixels / 0.45 M), at most 4
-  // (per-chunk harmonic groups make the short edge strips cheap: c2 measured
-  // best at K = 4 with 35 % edges, 1.45 -> 1.31 ms; c4 keeps K = 4 / 20 %)
-  int best = static_cast<int>(std::lround(std::sqrt(px / 0.3e6)));
-  best = std::max(1, std::min(best, 4));
-  if (const char* force = getenv("FBF_HOST_CHUNKS")) best = std::max(1, atoi(force));  // experiments
-  while (best > 1 && g->out_rows / best < 4 * W + 16) --best;
-  // the first strip's H2D and the last strip's D2H are not hidden: those two
-  // strips get 20 % of a middle strip's rows (measured: c2 K=3 2553 -> 2730,
-  // c4 K=4 1637 -> 1707 e2e Mpixel/s; FBF_HOST_EDGE overrides, experiments)
-  const long long e_default = px <= 16e6 ? 35 : 20;
-  const long long e = best >= 3 ? (getenv("FBF_HOST_EDGE") ? atoi(getenv("FBF_HOST_EDGE")) : e_default) : 100;
-  const long long wsum = 2 * e + 100LL * (best - 2);
-  auto cut = [&](int i) {  // cumulative weight of strips [0, i)
-    const long long w = i == 0 ? 0 : i == best ? wsum : e + 100LL * (i - 1);
-    return g->out_row0 + static_cast<int>(g->out_rows * w / wsum) / 16 * 16;
-  };
-  for (int i = 0; i < best; ++i) {
-    int o0 = cut(i);
-    int o1 = i + 1 == best ? g->out_row0 + g->out_rows : cut(i + 1);
-    if (i == 0) o0 = g->out_row0;
-    if (o1 <= o0) continue;
-    const int s0 = std::max(g->src_row0, std::max(0, o0 - W));
-    const int s1 = std::min(g->src_row0 + g->src_rows, std::min(g->height, o1 + W));
-    c.push_back({0, 1, o0, o1, s0, s1});
-  }
-  return c;
+int fbf_convolve_device(int width, int height, const double* profile, int radius, const float* src, float* dst,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+  return convolve_any<float>(width, height, profile, radius, src, dst, workspace, workspace_bytes,
+                             static_cast<cudaStream_t>(stream));
 }
 
-}  // namespace
-
-}  // extern "C"
-
-namespace {
-// Host-buffer entry of the recursive backend: whole images, fp64 inside,
-// T-typed host buffers in and out (the f64 entry keeps the reference's doubles).
-template <class T>
-int iir_host(const fbf_geometry* g, const fbf_filter* f, const T* src, T* dst, long long* bad_index) {
-  fbf_geometry gd = *g;
-  gd.src_pitch = g->width;
-  gd.dst_pitch = g->width;
-  gd.src_bstride = static_cast<long long>(g->src_rows) * g->width;
-  gd.dst_bstride = static_cast<long long>(g->out_rows) * g->width;
-  const size_t src_bytes = static_cast<size_t>(gd.src_bstride) * g->batch * sizeof(T);
-  const size_t dst_bytes = static_cast<size_t>(gd.dst_bstride) * g->batch * sizeof(T);
-  const size_t ws_bytes = iir_workspace_bytes(g, f->radius);
-  HostCtx* ctx = nullptr;
-  int rc = host_ctx(align256(src_bytes) + align256(dst_bytes) + ws_bytes + 256, ctx);
-  if (rc) return rc;
-  cudaStream_t st = ctx->st;
-  T* d_src = reinterpret_cast<T*>(ctx->buf);
-  T* d_dst = reinterpret_cast<T*>(ctx->buf + align256(src_bytes));
-  char* ws = ctx->buf + align256(src_bytes) + align256(dst_bytes);
-  unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(ws + ws_bytes);
-  for (int b = 0; b < g->batch; ++b)
-    FBF_CUDA(cudaMemcpy2DAsync(d_src + b * gd.src_bstride, g->width * sizeof(T), src + b * g->src_bstride,
-                               g->src_pitch * sizeof(T), g->width * sizeof(T), g->src_rows,
-                               cudaMemcpyHostToDevice, st));
-  FBF_CUDA(cudaMemsetAsync(d_bad, 0xFF, sizeof(unsigned long long), st));
-  rc = iir_bilateral<T, T>(&gd, f, d_src, d_dst, ws, ws_bytes, d_bad, st);
-  if (rc) {
-    cudaStreamSynchronize(st);
-    return rc;
-  }
-  for (int b = 0; b < g->batch; ++b)
-    FBF_CUDA(cudaMemcpy2DAsync(dst + b * g->dst_bstride, g->dst_pitch * sizeof(T), d_dst + b * gd.dst_bstride,
-                               g->width * sizeof(T), g->width * sizeof(T), g->out_rows, cudaMemcpyDeviceToHost,
-                               st));
-  unsigned long long bad = ~0ULL;
-  FBF_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
-  FBF_CUDA(cudaStreamSynchronize(st));
-  if (bad != ~0ULL) {
-    if (bad_index) *bad_index = static_cast<long long>(bad);
-    const long long per = static_cast<long long>(g->width) * g->height;
-    const long long inimg = static_cast<long long>(bad) % per;
-    return fail(FBF_EANOMALY, "bilateral_fast: numerical anomaly, denominator collapsed at pixel (" +
-                                  std::to_string(inimg % g->width) + ", " + std::to_string(inimg / g->width) + ")");
-  }
-  return FBF_OK;
-}
-}  // namespace
-
-extern "C" {
-
-int fbf_bilateral_fast_host(const fbf_geometry* g, const fbf_filter* f, const float* src,
-                            float* dst, int variant, long long* bad_index) {
-  int rc = check_geometry(g);
-  if (rc) return rc;
-  if ((rc = check_filter(f))) return rc;
-  if ((rc = check_halo(g, f->radius))) return rc;
-  int v = variant;
-  if (v == FBF_VARIANT_RECURSIVE) {
-    if (uses_iir(f)) return iir_host<float>(g, f, src, dst, bad_index);
-    v = FBF_VARIANT_FUSED;  // box windows and sigma < 2 stay direct (spatial.hpp:102-104)
-  }
-  if (v == FBF_VARIANT_FUSED && !fused_supported(f->radius, f->kind == FBF_SPATIAL_BOX)) v = FBF_VARIANT_NAIVE;
-  const std::vector<Chunk> chunks = plan_chunks(g, f->radius, v);
-  const int K = static_cast<int>(chunks.size());
-  // device buffers: dense copies of the source rows and output rows of the whole call
-  const long long sb = static_cast<long long>(g->src_rows) * g->width;  // per image
-  const long long db = static_cast<long long>(g->out_rows) * g->width;
-  const size_t src_bytes = static_cast<size_t>(sb) * g->batch * sizeof(float);
-  const size_t dst_bytes = static_cast<size_t>(db) * g->batch * sizeof(float);
-  auto chunk_geometry = [&](const Chunk& c) {
-    fbf_geometry gc = *g;
-    gc.batch = c.nb;
-    gc.src_row0 = c.s0;
-    gc.src_rows = c.s1 - c.s0;
-    gc.out_row0 = c.o0;
-    gc.out_rows = c.o1 - c.o0;
-    gc.src_pitch = g->width;
-    gc.dst_pitch = g->width;
-    gc.src_bstride = sb;
-    gc.dst_bstride = db;
-    return gc;
-  };
-  // Each chunk picks its own harmonic grouping from the cost model (short edge
-  // strips: more groups, so their kernels finish while the middle strip's
-  // copies run).  A chunk whose count differs from the whole call's sums its
-  // group planes in another order: equal to one launch to fp32 rounding, not
-  // bit for bit.  FBF_HOST_INHERIT_GROUPS=1 restores the whole call's count
-  // for every chunk (bit-identical to one launch).
-  static const bool inherit = getenv("FBF_HOST_INHERIT_GROUPS") != nullptr;
-  struct GroupsOverride {
-    explicit GroupsOverride(int g) { g_groups_override = g; }
-    ~GroupsOverride() { g_groups_override = 0; }
-  } groups_override(inherit ? harmonic_groups(g, f->radius, f->N + 1) : 0);
-  size_t ws_bytes = 0;
-  for (const Chunk& c : chunks) {
-    const fbf_geometry gc = chunk_geometry(c);
-    ws_bytes = std::max(ws_bytes, align256(layout_of(&gc, f->radius, v).total));
-  }
-  const int nws = K > 1 ? 2 : 1;
-  const size_t total = align256(src_bytes) + align256(dst_bytes) + nws * ws_bytes + align256(K * 8) + 256;
-  HostCtx* ctx = nullptr;
-  if ((rc = host_ctx(total, ctx))) return rc;
-  cudaStream_t sts[2] = {ctx->st, ctx->st2};
-  char* buf = ctx->buf;
-  float* d_src = reinterpret_cast<float*>(buf);
-  float* d_dst = reinterpret_cast<float*>(buf + align256(src_bytes));
-  char* ws0 = buf + align256(src_bytes) + align256(dst_bytes);
-  unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(ws0 + nws * ws_bytes);
-  if (K > 16) return fail(FBF_EINVAL, "bilateral_fast: too many pipeline chunks");
-  // Issue the whole call on the two streams (memset, per chunk H2D -> kernels
-  // -> D2H, join, collapse read-back); capturable into a CUDA graph.
-  auto issue = [&]() -> int {
-    cudaError_t e = cudaMemsetAsync(d_bad, 0xFF, K * sizeof(unsigned long long), sts[0]);
-    if (e == cudaSuccess && K > 1) e = cudaEventRecord(ctx->ev[1], sts[0]);
-    if (e == cudaSuccess && K > 1) e = cudaStreamWaitEvent(sts[1], ctx->ev[1], 0);
-    if (e != cudaSuccess) return cuda_fail(e, "memset");
-    int copied_hi = g->src_row0;  // row strips: source rows already on their way to the device
-    for (int k = 0; k < K; ++k) {
-      const Chunk& c = chunks[k];
-      cudaStream_t st = sts[k & 1];
-      // H2D: this chunk's images, or the source rows no earlier strip has copied
-      const int r0 = g->batch >= 2 || K == 1 ? c.s0 : std::max(c.s0, copied_hi);
-      // images stacked without gaps (whole rows, bstride = rows * pitch): one 2-D copy
-      const bool src_stacked = r0 == g->src_row0 && c.s1 == g->src_row0 + g->src_rows &&
-                               g->src_bstride == static_cast<long long>(g->src_rows) * g->src_pitch;
-      for (int b = c.b0; b < c.b0 + c.nb && r0 < c.s1; b += src_stacked ? c.nb : 1) {
-        e = cudaMemcpy2DAsync(d_src + b * sb + static_cast<long long>(r0 - g->src_row0) * g->width,
-                              g->width * sizeof(float),
-                              src + b * g->src_bstride + static_cast<long long>(r0 - g->src_row0) * g->src_pitch,
-                              g->src_pitch * sizeof(float), g->width * sizeof(float),
-                              src_stacked ? static_cast<size_t>(c.nb) * g->src_rows : c.s1 - r0,
-                              cudaMemcpyHostToDevice, st);
-        if (e != cudaSuccess) return cuda_fail(e, "H2D");
-      }
-      if (g->batch < 2 && K > 1) {
-        // the strip's upper halo rows came with the previous strip, on the other stream
-        if (k > 0 && c.s0 < copied_hi) e = cudaStreamWaitEvent(st, ctx->ev[(k - 1) & 1], 0);
-        if (e == cudaSuccess) e = cudaEventRecord(ctx->ev[k & 1], st);
-        if (e != cudaSuccess) return cuda_fail(e, "event");
-        copied_hi = std::max(copied_hi, c.s1);
-      }
-      const fbf_geometry gc = chunk_geometry(c);
-      const int rc2 = fbf_bilateral_fast_device(
-          &gc, f, d_src + c.b0 * sb + static_cast<long long>(c.s0 - g->src_row0) * g->width,
-          d_dst + c.b0 * db + static_cast<long long>(c.o0 - g->out_row0) * g->width,
-          ws0 + (k & 1) * (nws > 1 ? ws_bytes : 0), ws_bytes, d_bad + k, v, st);
-      if (rc2 != FBF_OK) return rc2;
-      const bool dst_stacked = c.o0 == g->out_row0 && c.o1 == g->out_row0 + g->out_rows &&
-                               g->dst_bstride == static_cast<long long>(g->out_rows) * g->dst_pitch;
-      for (int b = c.b0; b < c.b0 + c.nb; b += dst_stacked ? c.nb : 1) {
-        e = cudaMemcpy2DAsync(dst + b * g->dst_bstride + static_cast<long long>(c.o0 - g->out_row0) * g->dst_pitch,
-                              g->dst_pitch * sizeof(float),
-                              d_dst + b * db + static_cast<long long>(c.o0 - g->out_row0) * g->width,
-                              g->width * sizeof(float), g->width * sizeof(float),
-                              dst_stacked ? static_cast<size_t>(c.nb) * g->out_rows : c.o1 - c.o0,
-                              cudaMemcpyDeviceToHost, st);
-        if (e != cudaSuccess) return cuda_fail(e, "D2H");
-      }
-    }
-    if (K > 1) {
-      e = cudaEventRecord(ctx->join, sts[1]);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(sts[0], ctx->join, 0);
-      if (e != cudaSuccess) return cuda_fail(e, "join");
-    }
-    e = cudaMemcpyAsync(ctx->h_bad, d_bad, K * sizeof(unsigned long long), cudaMemcpyDeviceToHost, sts[0]);
-    return e == cudaSuccess ? FBF_OK : cuda_fail(e, "D2H");
-  };
-  // graph replay key: everything the issued work depends on
-  std::vector<unsigned char> key;
-  auto put = [&](const void* p, size_t n) {
-    const unsigned char* c = static_cast<const unsigned char*>(p);
-    key.insert(key.end(), c, c + n);
-  };
-  put(g, sizeof(*g));
-  put(&f->kind, sizeof(f->kind));
-  put(&f->radius, sizeof(f->radius));
-  put(&f->w0, sizeof(f->w0));
-  put(&f->N, sizeof(f->N));
-  put(&f->omega, sizeof(f->omega));
-  put(&f->max_pointwise_error, sizeof(f->max_pointwise_error));
-  put(&f->check_epsilon, sizeof(f->check_epsilon));
-  put(f->d, (f->N + 1) * sizeof(double));
-  put(f->profile, (2 * f->radius + 1) * sizeof(double));
-  put(&v, sizeof(v));
-  put(&src, sizeof(src));
-  put(&dst, sizeof(dst));
-  put(&ctx->buf, sizeof(ctx->buf));
-  auto pinned = [](const void* p) {
-    cudaPointerAttributes at{};
-    const bool ok = cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost;
-    cudaGetLastError();
-    return ok;
-  };
-  // graphs pay off for single-launch calls (c1 / c3 e2e +13-15 %); replaying the
-  // two-stream pipeline measured slower than issuing it (c2 -5 %)
-  static const bool graphs_env = !getenv("FBF_NO_GRAPH");
-  const bool graphs = graphs_env && K == 1;
-  static const bool graph_debug = getenv("FBF_GRAPH_DEBUG") != nullptr;
-  int out = FBF_OK;
-  if (graph_debug)
-    fprintf(stderr, "fbf host: K=%d cached=%d same_key=%d pinned=%d/%d\n", K, ctx->graph != nullptr,
-            key == ctx->graph_key, pinned(src), pinned(dst));
-  if (graphs && ctx->graph && key == ctx->graph_key) {
-    const cudaError_t e = cudaGraphLaunch(ctx->graph, sts[0]);
-    out = e == cudaSuccess ? FBF_OK : cuda_fail(e, "graph launch");
-  } else if (graphs && pinned(src) && pinned(dst)) {
-    // record this call as a graph (pageable host buffers cannot be captured)
-    cudaGraph_t graph = nullptr;
-    cudaError_t e = cudaStreamBeginCapture(sts[0], cudaStreamCaptureModeThreadLocal);
-    out = e == cudaSuccess ? issue() : cuda_fail(e, "capture");
-    if (e == cudaSuccess) e = cudaStreamEndCapture(sts[0], &graph);
-    cudaGraphExec_t exec = nullptr;
-    if (out == FBF_OK && e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
-    if (graph) cudaGraphDestroy(graph);
-    if (out == FBF_OK && e == cudaSuccess) {
-      if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
-      ctx->graph = exec;
-      ctx->graph_key = std::move(key);
-      e = cudaGraphLaunch(exec, sts[0]);
-      out = e == cudaSuccess ? FBF_OK : cuda_fail(e, "graph launch");
-    } else {  // capture not possible here: issue directly
-      if (graph_debug) fprintf(stderr, "fbf host: capture failed (%d, %s)\n", out, cudaGetErrorString(e));
-      if (exec) cudaGraphExecDestroy(exec);
-      cudaGetLastError();
-      out = issue();
-    }
-  } else {
-    out = issue();
-  }
-  cudaError_t e = cudaStreamSynchronize(sts[0]);
-  if (out == FBF_OK && e != cudaSuccess) out = cuda_fail(e, "sync");
-  if (out != FBF_OK) {
-    cudaStreamSynchronize(sts[1]);
-    return out;
-  }
-  // chunk-local image index -> the call's (the kernels number images from 0 per launch)
-  const unsigned long long per_img = static_cast<unsigned long long>(g->width) * g->height;
-  unsigned long long first_bad = ~0ULL;
-  for (int k = 0; k < K; ++k)
-    if (ctx->h_bad[k] != ~0ULL)
-      first_bad = std::min(first_bad, ctx->h_bad[k] + static_cast<unsigned long long>(chunks[k].b0) * per_img);
-  if (first_bad != ~0ULL) {
-    if (bad_index) *bad_index = static_cast<long long>(first_bad);
-    const long long inimg = static_cast<long long>(first_bad % per_img);
-    const long long x = inimg % g->width, y = inimg / g->width;
-    return fail(FBF_EANOMALY, "bilateral_fast: numerical anomaly, denominator collapsed at pixel (" +
-                                  std::to_string(x) + ", " + std::to_string(y) + ")");
-  }
-  return FBF_OK;
-}
-
-void fbf_release_host_buffers(void) {
-  if (g_host.graph) cudaGraphExecDestroy(g_host.graph);
-  if (g_host.buf) cudaFree(g_host.buf);
-  if (g_host.st) cudaStreamDestroy(g_host.st);
-  if (g_host.st2) cudaStreamDestroy(g_host.st2);
-  for (auto e : g_host.ev)
-    if (e) cudaEventDestroy(e);
-  if (g_host.join) cudaEventDestroy(g_host.join);
-  if (g_host.h_bad) cudaFreeHost(g_host.h_bad);
-  g_host = HostCtx{};
-  if (g_pinned) cudaFreeHost(g_pinned);
-  g_pinned = nullptr;
-  g_pinned_cap = 0;
-}
-
-int fbf_bilateral_fast_host_f64(const fbf_geometry* g, const fbf_filter* f, const double* src,
-                                double* dst, int variant, long long* bad_index) {
-  int rc = check_geometry(g);
-  if (rc) return rc;
-  if ((rc = check_filter(f))) return rc;  // validate before touching the device
-  if ((rc = check_halo(g, f->radius))) return rc;
-  if (variant == FBF_VARIANT_RECURSIVE && uses_iir(f)) return iir_host<double>(g, f, src, dst, bad_index);
-  fbf_geometry gd = *g;
-  gd.src_pitch = g->width;
-  gd.dst_pitch = g->width;
-  gd.src_bstride = static_cast<long long>(g->src_rows) * g->width;
-  gd.dst_bstride = static_cast<long long>(g->out_rows) * g->width;
-  const size_t ns = static_cast<size_t>(gd.src_bstride) * g->batch;
-  const size_t nd = static_cast<size_t>(gd.dst_bstride) * g->batch;
-  float* hs = nullptr;
-  if ((rc = host_staging((ns + nd) * sizeof(float), hs))) return rc;
-  float* hd = hs + ns;
-  for (int b = 0; b < g->batch; ++b)
-    for (int y = 0; y < g->src_rows; ++y)
-      for (int x = 0; x < g->width; ++x)
-        hs[b * gd.src_bstride + static_cast<long long>(y) * g->width + x] =
-            static_cast<float>(src[b * g->src_bstride + y * g->src_pitch + x]);
-  rc = fbf_bilateral_fast_host(&gd, f, hs, hd, variant, bad_index);
-  if (rc == FBF_OK)
-    for (int b = 0; b < g->batch; ++b)
-      for (int y = 0; y < g->out_rows; ++y)
-        for (int x = 0; x < g->width; ++x)
-          dst[b * g->dst_bstride + y * g->dst_pitch + x] =
-              hd[b * gd.dst_bstride + static_cast<long long>(y) * g->width + x];
-  return rc;
-}
-
-int fbf_convolve_device(int width, int height, const double* profile, int radius, const float* src,
-                        float* dst, void* workspace, size_t workspace_bytes, void* stream) {
-  if (width <= 0 || height <= 0) return fail(FBF_EINVAL, "convolve: empty plane");
-  if (radius < 0 || radius > kMaxW) return fail(FBF_EUNSUPPORTED, "convolve: radius outside [0, 64]");
-  const size_t need = static_cast<size_t>(width) * height * sizeof(float);
-  if (!workspace || workspace_bytes < need) return fail(FBF_EINVAL, "convolve: workspace too small");
-  Taps K;
-  std::memset(&K, 0, sizeof(K));
-  K.W = radius;
-  for (int j = 0; j <= radius; ++j) {
-    K.t[j] = static_cast<float>(profile[radius + j]);
-  }
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  float* tmp = static_cast<float*>(workspace);
-  const long long n = static_cast<long long>(width) * height;
-  conv_rows_f32<<<grid_for(n, 256), 256, 0, st>>>(src, tmp, width, height, K);
-  conv_cols_f32<<<grid_for(n, 256), 256, 0, st>>>(tmp, dst, width, height, K);
-  FBF_CUDA(cudaGetLastError());
-  return FBF_OK;
-}
-
-int fbf_convolve_host_f64(int width, int height, const double* profile, int radius,
-                          const double* src, double* dst) {
-  if (width <= 0 || height <= 0) return fail(FBF_EINVAL, "convolve: empty plane");
-  const size_t n = static_cast<size_t>(width) * height;
-  float* h = nullptr;
-  HostCtx* ctx = nullptr;
-  int rc = host_staging(n * sizeof(float), h);
-  if (rc == FBF_OK) rc = host_ctx(3 * align256(n * 4), ctx);
-  if (rc) return rc;
-  cudaStream_t st = ctx->st;
-  char* d = ctx->buf;
-  cudaError_t e = cudaSuccess;
-  {
-    for (size_t i = 0; i < n; ++i) h[i] = static_cast<float>(src[i]);
-    float* ds = reinterpret_cast<float*>(d);
-    float* dd = reinterpret_cast<float*>(d + align256(n * 4));
-    void* ws = d + 2 * align256(n * 4);
-    e = cudaMemcpyAsync(ds, h, n * 4, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) {
-      rc = fbf_convolve_device(width, height, profile, radius, ds, dd, ws, align256(n * 4), st);
-      if (rc == FBF_OK) {
-        e = cudaMemcpyAsync(h, dd, n * 4, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        if (e != cudaSuccess) rc = cuda_fail(e, "convolve D2H");
-        else
-          for (size_t i = 0; i < n; ++i) dst[i] = h[i];
-      }
-    } else {
-      rc = cuda_fail(e, "convolve H2D");
-    }
-  }
-  cudaStreamSynchronize(st);
-  return rc;
+int fbf_convolve_device_f64(int width, int height, const double* profile, int radius, const double* src,
+                            double* dst, void* workspace, size_t workspace_bytes, void* stream) {
+  return convolve_any<double>(width, height, profile, radius, src, dst, workspace, workspace_bytes,
+                              static_cast<cudaStream_t>(stream));
 }
 
 int fbf_probe_fma_peak(double* ops_per_s, double* sm_mhz, void* stream) {
@@ -1281,12 +933,11 @@ int fbf_probe_fma_peak(double* ops_per_s, double* sm_mhz, void* stream) {
   cudaEventSynchronize(e1);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
-  long long* h = new long long[blocks];
-  cudaMemcpyAsync(h, cyc, blocks * sizeof(long long), cudaMemcpyDeviceToHost, st);
+  std::vector<long long> h(blocks);
+  cudaMemcpyAsync(h.data(), cyc, blocks * sizeof(long long), cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
   long long mx = 0;
   for (int i = 0; i < blocks; ++i) mx = std::max(mx, h[i]);
-  delete[] h;
   cudaFreeAsync(out, st);
   cudaFreeAsync(cyc, st);
   cudaEventDestroy(e0);

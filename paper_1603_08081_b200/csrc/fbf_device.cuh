@@ -61,6 +61,44 @@ __device__ __forceinline__ p2 mul2(p2 a, p2 b) {
   return r;
 }
 
+// int32 pair <-> p2 and lane-wise int32 add (the fixed-point (Q, P) sums)
+__device__ __forceinline__ p2 pki(int lo, int hi) { return pk(__int_as_float(lo), __int_as_float(hi)); }
+__device__ __forceinline__ p2 iadd2(p2 a, p2 b) {
+  float al, ah, bl, bh;
+  upk(a, al, ah);
+  upk(b, bl, bh);
+  return pki(__float_as_int(al) + __float_as_int(bl), __float_as_int(ah) + __float_as_int(bh));
+}
+// the term (x_q, x_p) (already scaled by 2^aq, 2^ap) rounded to integers
+__device__ __forceinline__ p2 to_fixed(p2 x) {
+  float xq, xp;
+  upk(x, xq, xp);
+  return pki(__float2int_rn(xq), __float2int_rn(xp));
+}
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }  // |e| <= 126
+
+// Fixed-point grids of the (Q, P) sums (fbf_params.h Harmonics): 2^aq for Q,
+// 2^ap for P with ap = aq - k, 2^k >= max |f'| of the call (fmax word, float
+// bits, written by the prep kernel), k >= 7.
+struct FixedScale {
+  float sq, sp;  // 2^aq, 2^ap  (term scales)
+  float iq, ip;  // 2^-aq, 2^-ap (back to values)
+};
+__device__ __forceinline__ FixedScale fixed_scale(int aq, const unsigned* fmax) {
+  const unsigned b = fmax ? *fmax : 0u;
+  int k = static_cast<int>((b >> 23) & 0xffu) - 127 + ((b & 0x7fffffu) != 0u);  // ceil(log2 fmax)
+  k = min(max(k, 7), 60);
+  const int ap = aq - k;
+  return FixedScale{pow2f(aq), pow2f(ap), pow2f(-aq), pow2f(-ap)};
+}
+// (Q, P) values of a fixed-point pair
+__device__ __forceinline__ void from_fixed(p2 v, const FixedScale& fs, float& Q, float& P) {
+  float a, b;
+  upk(v, a, b);
+  Q = __int2float_rn(__float_as_int(a)) * fs.iq;
+  P = __int2float_rn(__float_as_int(b)) * fs.ip;
+}
+
 // cp.async (LDGSTS) helpers: 8-byte global -> shared copies in commit groups.
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
@@ -99,6 +137,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "}\n" ::"r"(smem_addr(bar)),
       "r"(parity)
       : "memory");
+}
+// order this thread's earlier generic-proxy global writes before later
+// async-proxy (TMA) reads of the same addresses, across a barrier
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 // 3-D tile load (x, y, image) of a CUtensorMap into shared memory
 __device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, uint64_t* bar, int x, int y,

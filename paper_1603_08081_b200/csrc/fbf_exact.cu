@@ -16,7 +16,8 @@ namespace {
 constexpr int TX = 16, TY = 16;
 
 // one thread per output pixel; the block's (16+2W)^2 input tile in smem (fp64)
-__global__ void exact_kernel(const float* __restrict__ src, double* __restrict__ dst, int width, int height,
+template <class Tin>
+__global__ void exact_kernel(const Tin* __restrict__ src, double* __restrict__ dst, int width, int height,
                              int src_row0, int out_row0, int out_rows, const double* __restrict__ prof_g, int W,
                              int family, double inv_scale) {
   extern __shared__ double tile[];
@@ -51,24 +52,53 @@ __global__ void exact_kernel(const float* __restrict__ src, double* __restrict__
   dst[static_cast<long long>(y - out_row0) * width + x] = num / den;
 }
 
-}  // namespace
-
-extern "C" int fbf_bilateral_exact_device(const fbf_geometry* g, const double* profile, int radius, int family,
-                                          double sigma_r, const float* src, double* dst, void* stream) {
+template <class Tin>
+int exact_any(const fbf_geometry* g, const double* profile, int radius, int family, double sigma_r, const Tin* src,
+              double* dst, cudaStream_t st) {
   if (!g || g->width <= 0 || g->height <= 0 || g->batch != 1 || radius < 1 || radius > 64 || !(sigma_r > 0.0))
     return FBF_EINVAL;
   double* d_prof = nullptr;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cudaMallocAsync(reinterpret_cast<void**>(&d_prof), sizeof(double) * (2 * radius + 1), st) != cudaSuccess)
     return FBF_ECUDA;
   cudaMemcpyAsync(d_prof, profile, sizeof(double) * (2 * radius + 1), cudaMemcpyHostToDevice, st);
   const double inv_scale =
       family == FBF_RANGE_EXPONENTIAL ? 1.0 / sigma_r : 1.0 / (2.0 * sigma_r * sigma_r);  // kernels.hpp:83-85
   const size_t smem = sizeof(double) * ((TX + 2 * radius) * (TY + 2 * radius) + 2 * radius + 1);
-  cudaFuncSetAttribute(exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaFuncSetAttribute(exact_kernel<Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   const dim3 grid((g->width + TX - 1) / TX, (g->out_rows + TY - 1) / TY);
-  exact_kernel<<<grid, dim3(TX, TY), smem, st>>>(src, dst, g->width, g->height, g->src_row0, g->out_row0,
-                                                 g->out_rows, d_prof, radius, family, inv_scale);
+  exact_kernel<Tin><<<grid, dim3(TX, TY), smem, st>>>(src, dst, g->width, g->height, g->src_row0, g->out_row0,
+                                                      g->out_rows, d_prof, radius, family, inv_scale);
   cudaFreeAsync(d_prof, st);
   return cudaGetLastError() == cudaSuccess ? FBF_OK : FBF_ECUDA;
+}
+
+}  // namespace
+
+extern "C" int fbf_bilateral_exact_device(const fbf_geometry* g, const double* profile, int radius, int family,
+                                          double sigma_r, const float* src, double* dst, void* stream) {
+  return exact_any<float>(g, profile, radius, family, sigma_r, src, dst, static_cast<cudaStream_t>(stream));
+}
+
+// bilateral_exact of a whole fp64 host image (the C++ API's Gaussian and
+// exponential range kernels): H2D, the kernel above in fp64, D2H.
+extern "C" int fbf_bilateral_exact_host_f64(int width, int height, const double* profile, int radius, int family,
+                                            double sigma_r, const double* src, double* dst) {
+  if (width <= 0 || height <= 0) return FBF_EINVAL;
+  fbf_geometry g;
+  fbf_geometry_whole(&g, width, height, 1);
+  const size_t n = static_cast<size_t>(width) * height;
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return FBF_ECUDA;
+  double* buf = nullptr;
+  int rc = FBF_ECUDA;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&buf), 2 * n * sizeof(double), st) == cudaSuccess) {
+    rc = cudaMemcpyAsync(buf, src, n * sizeof(double), cudaMemcpyHostToDevice, st) == cudaSuccess ? FBF_OK : FBF_ECUDA;
+    if (rc == FBF_OK) rc = exact_any<double>(&g, profile, radius, family, sigma_r, buf, buf + n, st);
+    if (rc == FBF_OK && cudaMemcpyAsync(dst, buf + n, n * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      rc = FBF_ECUDA;
+    cudaFreeAsync(buf, st);
+  }
+  if (cudaStreamSynchronize(st) != cudaSuccess) rc = FBF_ECUDA;
+  cudaStreamDestroy(st);
+  return rc;
 }

@@ -257,8 +257,8 @@ template <class C>
 struct Pending {
   static constexpr int KH = C::KC / 2;
   p2 part[C::KC];  // c * acc (half A) or s * acc (half B), rows gi .. gi+KC-1
-  p2 pq[KH];       // running (Q, P) of this lane's output rows (0 at the first harmonic)
-  p2 dd;           // (d_n, d_n)
+  p2 pq[KH];       // running fixed-point (Q, P) of this lane's output rows (0 at the first harmonic)
+  p2 dd;           // (d_n 2^aq, d_n 2^ap)
   p2* dst;         // (Q, P) of this lane's first output row; rows A.pq_cols apart
   int nh;          // rows this lane stores (<= 0: nothing pending)
   // output row k of this lane: (q, p) = own half + partner's half
@@ -267,9 +267,10 @@ struct Pending {
     const p2 own = h ? part[KH + k] : part[k];
     return add2(own, __shfl_xor_sync(0xffffffffu, send, 16));
   }
-  // (Q, P) += d_n (q, p)
+  // (Q, P) += round(d_n (q, p)) on the fixed-point grid (exact integer sum)
+  __device__ __forceinline__ p2 accumulate(int k, p2 qpk) const { return iadd2(pq[k], to_fixed(mul2(dd, qpk))); }
   __device__ __forceinline__ void finish(int k, int h, int stride) const {
-    const p2 v = fma2(dd, qp(k, h), pq[k]);
+    const p2 v = accumulate(k, qp(k, h));
     if (k < nh) dst[k * stride] = v;
   }
 };
@@ -376,7 +377,8 @@ template <class C>
 __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restrict__ R,
                                          const float* __restrict__ CS, const p2* __restrict__ pqs,
                                          const Unit& u, int o, int base, int dn_idx, bool first, bool divide,
-                                         bool defer, const ModNext<C>& next, PhaseClock& clk, Pending<C>& pd) {
+                                         bool defer, const ModNext<C>& next, PhaseClock& clk, Pending<C>& pd,
+                                         const FixedScale& fs) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int h = lane >> 4;
   // warp -> (column chunk, run) as in the row pass's (chunk, row group): the
@@ -461,7 +463,7 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
   // box: both passes summed unweighted; the weight (1/(2W+1))^2 = w0 joins d_n here
   // d_n (dn_idx = n - d_base: the launch's coefficient block)
   const float dn = C::BOX ? A.h.d[dn_idx] * (A.k.box_tap * A.k.box_tap) : A.h.d[dn_idx];
-  pd.dd = pk(dn, dn);
+  pd.dd = pk(dn * fs.sq, dn * fs.sp);  // exact: powers of two
   if (!divide) {
     pd.dst = reinterpret_cast<p2*>(A.pq) +
              ((blockIdx.y * A.g.batch + u.b) * static_cast<long long>(A.g.out_rows) + (rr - A.g.out_row0)) *
@@ -486,9 +488,8 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
 #pragma unroll
   for (int k = 0; k < KH; ++k) {
     if (k < nh) {
-      const p2 acc2 = fma2(pd.dd, qp[k], pd.pq[k]);
       float Q, P;
-      upk(acc2, Q, P);
+      from_fixed(pd.accumulate(k, qp[k]), fs, Q, P);
       if (!(fabsf(Q) >= A.h.q_floor) && A.bad) {
         const unsigned long long lin =
             static_cast<unsigned long long>(u.b) * A.g.full_height * A.g.width +
@@ -520,6 +521,7 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
   unsigned ph_uf = 0;  // phase parity of the next completion of the copy barrier
   Pending<C> pd;
   pd.nh = 0;
+  const FixedScale fs = fixed_scale(A.h.aq, A.fmax);
   PhaseClock clk;
   clk.start();
 
@@ -636,12 +638,17 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
           // two steps (nsteps > 2; the generic-proxy stores keep the same
           // distance to the next harmonic's async-proxy (Q, P) load as before)
           const bool defer = C::DEFER && more && !divide && nsteps > 2;
-          col_pass<C>(A, R, CS, pqs, u, o, base, n - A.h.d_base, first, divide, defer, next, clk, pd);
+          col_pass<C>(A, R, CS, pqs, u, o, base, n - A.h.d_base, first, divide, defer, next, clk, pd, fs);
           clk.mark(7);
         } else {
           modulate_rows<C>(stage, next.M, rows2, next.n);
           clk.mark(6);
         }
+        // The (Q, P) rows stored this step (generic proxy: deferred finishes in
+        // this step's row pass, immediate ones in its column pass) are read
+        // back by a TMA load (async proxy) in the next harmonic: order them
+        // before the S1 barrier that precedes any such load.
+        fence_proxy_async_global();
         clk.step();
         ++mk;
       }

@@ -10,7 +10,8 @@ namespace fbf {
 constexpr int kMaxD = 256;     // harmonic coefficients carried by one fused launch
 constexpr int kMaxN = 65535;   // highest harmonic accepted (larger N: several fused launches)
 constexpr int kFusedTW = 64;  // column-strip width of the fused kernel (workspace layout)
-constexpr int kMaxW = 64;   // largest spatial radius supported by the fused/naive paths
+constexpr int kMaxWFused = 64;      // taps carried in the fused kernel's parameter block (W <= this)
+constexpr int kMaxRadius = 1 << 20;  // largest spatial radius accepted (naive chain / convolve: taps in memory)
 
 struct Pair {
   float x, y;
@@ -32,8 +33,19 @@ struct Geometry {
   int dst_pitch;          // elements between rows of dst (row 0 = global out_row0)
 };
 
+// Fixed-point (Q, P): every harmonic's term d_n (q_n, p_n) is rounded once, in
+// fp32, to integers on the grid 2^-aq (Q) and 2^-ap (P) and summed as int32.
+// Integer sums are exact, so the result does not depend on how the harmonics
+// are split among CTA groups, launches, pipeline chunks or GPUs (SPEC.md:300,
+// "accumulation order ... independent of pixel-level parallelism").  aq comes
+// from D = sum |d_n| (host, fill_harmonics): |Q| and every partial sum stay
+// below 2^31 * 2^-aq.  ap = aq - k with 2^k >= max |f'| (k >= 7), from the
+// prep kernel's max |f - shift| of the call (fmax word in the workspace): for
+// 8-bit images k = 7 in every partition, so strips, batches and the whole
+// image agree bit for bit.
 struct Harmonics {
   int N;
+  int aq;              // Q grid exponent (see above)
   int d_base;          // d[i] is the coefficient of harmonic d_base + i
   float d[kMaxD];      // cosine coefficients d_base .. d_base + kMaxD - 1 (fp32)
   double turns_per_unit;  // omega / (2 pi): phase in turns per intensity unit
@@ -45,7 +57,7 @@ struct Taps {
   int W;
   int box;                // 1: uniform box window (running-sum path)
   float box_tap;          // 1/(2W+1)
-  float t[kMaxW + 1];     // tap |j| (spatial.hpp profile[W+j]); broadcast to both FFMA2 lanes
+  float t[kMaxWFused + 1];     // tap |j| (spatial.hpp profile[W+j]); broadcast to both FFMA2 lanes
 };
 
 // Fused path: the prep kernel writes a mirror-PADDED (u, f') image per image,
@@ -68,7 +80,8 @@ struct FusedArgs {
   Taps k;
   const int2* uf;          // prep output: (u = phase increment, f' bits)
   float* dst;
-  Pair* pq;                // workspace: per output pixel (Q, P), out_rows x width per image
+  Pair* pq;                // workspace: per output pixel (Q, P) as an int32 pair (fixed point), out_rows x width per image
+  const unsigned* fmax;    // workspace header: max |f'| of the call as float bits (prep)
   unsigned long long* bad; // min linear index (b*H*W + y*W + x) of a collapsed denominator
   int strips;              // ceil(width / TW)
   long long total;         // batch * strips * out_rows

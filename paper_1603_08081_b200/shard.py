@@ -83,7 +83,9 @@ def harmonic_split_filter(src, geo, spatial, approx, workspace, dst, bad, group=
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     n_lo, n_hi = harmonic_range(approx.N, world, rank)
     st = torch.cuda.current_stream().cuda_stream
-    pq = torch.zeros((geo.batch, geo.out_rows, geo.width, 2), dtype=torch.float32, device=src.device)
+    # exact fp64 partial sums (multiples of the call's fixed-point grid): the
+    # all-reduce adds them exactly, so the result is the single-GPU bits
+    pq = torch.zeros((geo.batch, geo.out_rows, geo.width, 2), dtype=torch.float64, device=src.device)
     prepare_device(src.data_ptr(), geo, spatial, approx, workspace.data_ptr(), workspace.numel(), st, variant,
                    check_epsilon)
     if n_hi > n_lo:

@@ -59,11 +59,12 @@ def test_c5_batch_images(oracle):
     for k, i in enumerate(idx):
         ref = oracle_rows(oracle, batch[k], s, a, True, 500, 532)
         assert maxabs(gpu[k, 500:532], ref) <= TOL
-        # batched result == the image filtered alone, to fp32 rounding of the
-        # group sums (the host entry runs a lone 1 Mpixel image as two strips,
-        # each with its own harmonic grouping; bit for bit where they agree)
+        # batched result == the image filtered alone, bit for bit: the host
+        # entry runs a lone 1 Mpixel image as two pipeline strips with their own
+        # harmonic grouping, and the fixed-point (Q, P) sums make the result
+        # independent of that partition
         alone = fb.bilateral_fast(batch[k], s, a)
-        assert maxabs(alone, gpu[k]) <= 2e-4
+        assert np.array_equal(alone, gpu[k])
 
 
 @pytest.mark.parametrize("name", list(CONFIGS))
