@@ -31,6 +31,7 @@
 
 #include "fbf_device.cuh"
 #include "fbf_params.h"
+#include "fbf_tuning.h"
 
 namespace fbf {
 
@@ -692,13 +693,7 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
   a.total = static_cast<long long>(a.g.batch) * a.strips * a.g.out_rows;
   // a unit's prologue row-passes 2W rows without a column pass or demodulation
   // (~55 % of a full row's cost, measured: FBF_UNIT_COST_PCT sweep)
-  {
-    static const int pct = [] {
-      const char* e = getenv("FBF_UNIT_COST_PCT");
-      return e ? atoi(e) : 55;
-    }();
-    a.unit_cost = 2 * W * pct / 100;
-  }
+  a.unit_cost = static_cast<int>(2 * W * FBF_TUNABLE(UNIT_COST_FRAC, kUnitCostFrac));
   cudaError_t e = encode_tile_3d(&a.tm_uf, a.uf, static_cast<unsigned long long>(a.pq_cols + 2 * W),
                                  static_cast<unsigned long long>(a.g.out_rows + 2 * W),
                                  static_cast<unsigned long long>(a.g.batch), C::MW, C::G);
@@ -743,12 +738,16 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
 
 // Small (128 threads, G=16, two CTAs per SM) for W <= 9, big (256 threads,
 // G=32, one CTA per SM) otherwise -- measured, profiles/r01_cfg_compare.txt.
-// FBF_FUSED_CFG=small|big overrides where both fit (experiments).
+// FBF_FUSED_CFG=small|big overrides where both fit (experiment build only).
 template <int W, bool BOX = false>
 cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
   using Small = FusedCfg<W, 64, 16, 16, 16, 128, BOX>;
   using Big = FusedCfg<W, 64, 32, 16, 16, 256, BOX>;
+#ifdef FBF_EXPERIMENTS
   const char* env = getenv("FBF_FUSED_CFG");
+#else
+  const char* env = nullptr;
+#endif
   if constexpr (Small::smem_bytes <= 113 * 1024) {  // two 128-thread CTAs per SM
     const bool big = env ? env[0] == 'b' : !(W <= 9);
     if (!big || !Big::FITS) return launch_cfg<Small>(a, st, grid_out);
