@@ -736,11 +736,35 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
   return cudaGetLastError();
 }
 
+}  // namespace fbf
+#include "fbf_fused2.cuh"
+namespace fbf {
+
+#ifndef FBF_V2
+#define FBF_V2 0
+#endif
+// v2 schedule (fbf_fused2.cuh): small CTAs (two per SM) for W <= 9, big where
+// its tiles fit, else small with one CTA per SM
+template <int W, bool BOX>
+cudaError_t launch_w2(const FusedArgs& a, cudaStream_t st, int* grid_out) {
+  using Small = FusedCfg<W, 64, 16, 16, 16, 128, BOX>;
+  using Big = FusedCfg<W, 64, 32, 16, 16, 256, BOX>;
+  if constexpr (W <= 9 && V2<Small>::FITS2) {
+    return launch_cfg2<Small>(a, st, grid_out);
+  } else if constexpr (V2<Big>::FITS) {
+    return launch_cfg2<Big>(a, st, grid_out);
+  } else if constexpr (V2<Small>::FITS) {
+    return launch_cfg2<Small>(a, st, grid_out);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+}
+
 // Small (128 threads, G=16, two CTAs per SM) for W <= 9, big (256 threads,
 // G=32, one CTA per SM) otherwise -- measured, profiles/r01_cfg_compare.txt.
 // FBF_FUSED_CFG=small|big overrides where both fit (experiment build only).
-template <int W, bool BOX = false>
-cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
+template <int W, bool BOX>
+cudaError_t launch_w1(const FusedArgs& a, cudaStream_t st, int* grid_out) {
   using Small = FusedCfg<W, 64, 16, 16, 16, 128, BOX>;
   using Big = FusedCfg<W, 64, 32, 16, 16, 256, BOX>;
 #ifdef FBF_EXPERIMENTS
@@ -760,6 +784,14 @@ cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
     (void)env;
     return cudaErrorInvalidValue;
   }
+}
+
+template <int W, bool BOX = false>
+cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
+  if constexpr (FBF_V2)
+    return launch_w2<W, BOX>(a, st, grid_out);
+  else
+    return launch_w1<W, BOX>(a, st, grid_out);
 }
 
 }  // namespace fbf

@@ -44,7 +44,8 @@ def main():
          check_epsilon=False)
     if quick:
         return
-    case("W=30 (128 thr, 1/SM)", img, g(10.0), fb.fit_fixed(fb.RANGE_GAUSSIAN, 20.0, 255, 8))
+    case("W=30 (128 thr, 1/SM)", img, g(10.0), fb.fit_fixed(fb.RANGE_GAUSSIAN, 20.0, 255, 20),
+         check_epsilon=False)
     # tall narrow: many units per CTA and harmonic groups
     tall = fb.synth_image(5, 64, 700, 3, 10.0)
     case("W=12 tall (groups)", tall, g(4.0), fb.fit_fixed(fb.RANGE_GAUSSIAN, 25.0, 255, 16))
