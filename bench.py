@@ -525,7 +525,7 @@ def main():
             roof = {
                 "bound": "fp32_fma", "achieved": achieved, "peak": peak, "unit": "Tops/s",
                 "frac": achieved / peak, "traffic": load_traffic(cfg.name, args.variant),
-                "kernel": "fbf::fused_kernel", "kernel_ms": fused_ms, "prep_ms": prep_ms,
+                "kernel": "fbf::n0_plane_kernel + fbf::fused_kernel (+ finish_groups)", "kernel_ms": fused_ms, "prep_ms": prep_ms,
                 "ops_per_pixel": cfg.ops_per_pixel(),
                 "peak_source": f"measured in this run: FFMA2 probe fbf_probe_fma_peak at {peak_mhz:.0f} MHz "
                                "(128 FP32 lanes x 148 SMs); ops = FP32 FMA-pipe lane ops (FFMA/FMUL/FADD = 1)",

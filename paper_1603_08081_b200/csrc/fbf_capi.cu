@@ -62,10 +62,18 @@ namespace {
 
 // max |f'| of the call into the workspace header (fixed-point P grid,
 // fbf_params.h): one atomic per warp
+// max |f'| of the call: warp shuffle, then one shared-memory and one global
+// atomic per CTA (same-address global atomics per warp serialised in L2 and
+// were most of the prep kernel's time: c2 56 us -> see profiles/r02_notes.md)
 __device__ __forceinline__ void note_fmax(float m, unsigned* fmax) {
+  __shared__ unsigned cta_max;
+  if (threadIdx.x == 0) cta_max = 0u;
+  __syncthreads();
 #pragma unroll
   for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(fmax, __float_as_uint(m));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(&cta_max, __float_as_uint(m));
+  __syncthreads();
+  if (threadIdx.x == 0 && cta_max) atomicMax(fmax, cta_max);
 }
 
 __device__ __forceinline__ int2 phase_of(float f, double turns_scaled, float shift, float& m) {
@@ -622,14 +630,46 @@ int prepare_common(const fbf_geometry* gp, const fbf_filter* f, void* workspace,
   return FBF_OK;
 }
 
+// The n = 0 term of the fused path as its own single-plane filter.  At n = 0
+// the modulation is exact (c = 1, s = 0), so the harmonic's four planes reduce
+// to one: (q, p) = (conv(1), conv(f')) = (1, conv(f')) -- taps sum to one and
+// mirror padding keeps it so (bilateral.hpp:126-144 with n = 0).  Filtering
+// it inside the fused kernel would cost a full harmonic (four planes, halo
+// modulation, demodulation); here it is one separable FIR of f' read from the
+// padded (u, f') image, rounded to the same fixed-point grid as every other
+// term and written as group plane 0, onto which the fused kernel's group 0
+// accumulates harmonics 1..N.  The fixed-point sum is exact, so where the
+// n = 0 term is computed does not change the result's bits.
+//
+// Tile: 64 output columns x 32 output rows per CTA, 256 threads; smem holds the
+// (32+2W) x (64+2W) input tile and the row-filtered (32+2W) x 64 tile.
+// (kernel: n0_plane_kernel in fbf_fused.cuh, one instance per radius)
+cudaError_t launch_n0_plane(const FusedArgs& a_in, cudaStream_t st) {
+  FusedArgs a = a_in;
+  a.n0_only = 1;
+  return launch_fused(a, st, nullptr);
+}
+
 // Fused launches over harmonics [n_lo, n_hi): one launch when the range fits
 // the kMaxD coefficients of a parameter block (the common case, N < 256),
 // otherwise consecutive launches of kMaxD harmonics that keep accumulating
 // into the (Q, P) planes, the last one dividing unless `partial`.  Returns
 // the number of (Q, P) group planes left for finish_groups (1: none needed).
 int launch_fused_range(const FusedArgs& base, const fbf_filter* f, int n_lo, int n_hi, int groups, bool partial,
-                       cudaStream_t st, cudaError_t* err) {
+                       cudaStream_t st, cudaError_t* err, bool* divided = nullptr) {
+  if (divided) *divided = false;
   FusedArgs A = base;
+  // n = 0 as a single-plane filter (n0_plane_kernel) into group plane 0; the
+  // fused kernel then starts at n = 1 with group 0 accumulating onto it
+  // (always, so the n = 0 term has the same bits in every harmonic partition)
+  if (n_lo == 0) {
+    A.h.d[0] = static_cast<float>(f->d[0]);
+    *err = launch_n0_plane(A, st);
+    if (*err != cudaSuccess) return 0;
+    n_lo = 1;
+    A.acc_group0 = 1;
+    if (n_hi == 1) return 1;  // N = 0: plane 0 holds the sums; the caller divides
+  }
   const bool one = n_hi - n_lo <= kMaxD;
   A.groups = one ? std::max(1, std::min(groups, n_hi - n_lo)) : 1;
   for (int c0 = n_lo; c0 < n_hi; c0 += kMaxD) {
@@ -643,6 +683,7 @@ int launch_fused_range(const FusedArgs& base, const fbf_filter* f, int n_lo, int
     *err = launch_fused(A, st, nullptr);
     if (*err != cudaSuccess) return 0;
   }
+  if (divided) *divided = !A.partial;
   return A.groups;
 }
 
@@ -773,7 +814,10 @@ int fbf_prepare_device(const fbf_geometry* gp, const fbf_filter* f, const float*
     const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
     const int pairs = (cols + 2 * W) / 2;  // cols is a multiple of 64: even row length
     const long long rows = static_cast<long long>(P.G.out_rows + 2 * W) * P.G.batch;
-    const dim3 grid((pairs + 127) / 128, static_cast<unsigned>(std::min(rows, 65535LL)), 1);
+    // a few waves of CTAs in a grid-stride loop over rows (one fmax atomic per CTA)
+    const unsigned bx = static_cast<unsigned>((pairs + 127) / 128);
+    const long long by = std::max(1LL, std::min(rows, (148LL * 16 + bx - 1) / bx));
+    const dim3 grid(bx, static_cast<unsigned>(by), 1);
     prep_padded_kernel<<<grid, 128, 0, st>>>(src, P.uf, P.G, W, cols, scale, P.H.shift, P.fmax);
   } else {
     const long long src_px = static_cast<long long>(P.G.batch) * P.G.src_rows * P.G.width;
@@ -793,10 +837,11 @@ int fbf_filter_prepared_device(const fbf_geometry* gp, const fbf_filter* f, floa
   if (P.variant == FBF_VARIANT_FUSED) {
     const FusedArgs A = fused_args(P, dst, d_bad);
     cudaError_t e = cudaSuccess;
+    bool divided = false;
     const int groups =
-        launch_fused_range(A, f, 0, P.H.N + 1, harmonic_groups(gp, f->radius, P.H.N + 1), false, st, &e);
+        launch_fused_range(A, f, 0, P.H.N + 1, harmonic_groups(gp, f->radius, P.H.N + 1), false, st, &e, &divided);
     FBF_CUDA(e);
-    if (groups > 1) {
+    if (!divided) {
       const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
       const long long plane = static_cast<long long>(P.G.batch) * P.G.out_rows * cols;
       finish_groups<<<rows_grid(P.G), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), groups, P.H.N + 1, plane,
@@ -887,9 +932,11 @@ int fbf_launches_per_call(const fbf_geometry* g, const fbf_filter* f, int varian
     variant = FBF_VARIANT_FUSED;
   }
   if (variant == FBF_VARIANT_FUSED && fused_ok(f)) {
-    const int chunks = (f->N + kMaxD) / kMaxD;  // fused launches of <= kMaxD harmonics
-    if (chunks > 1) return 1 + chunks;
-    return std::min(harmonic_groups(g, f->radius, f->N + 1), f->N + 1) > 1 ? 3 : 2;  // prep, fused (, group sum)
+    // prep, the n = 0 plane (N >= 1), fused launches of <= kMaxD harmonics (, group sum)
+    if (f->N == 0) return 3;  // prep, n = 0 plane, divide
+    const int chunks = (f->N - 1 + kMaxD) / kMaxD;
+    if (chunks > 1) return 2 + chunks;
+    return 3 + (std::min(harmonic_groups(g, f->radius, f->N + 1), f->N) > 1 ? 1 : 0);
   }
   const int tap_uploads = (2 * f->radius + 1 + kTapChunk - 1) / kTapChunk;
   return 1 + tap_uploads + 4 * (f->N + 1) + 1;

@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
   if (nb >= ne) return;
   // the harmonic whose (Q, P) initialises the planes (none for a chained launch
   // that accumulates onto an earlier one)
-  const int n_first = A.accumulate ? -1 : nb;
+  const int n_first = (A.accumulate || (A.acc_group0 && blockIdx.y == 0)) ? -1 : nb;
 
   const long long total = A.total;
   // CTA ranges in (strip, row) space, with the row rounded down to a multiple
@@ -736,35 +736,204 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
   return cudaGetLastError();
 }
 
-}  // namespace fbf
-#include "fbf_fused2.cuh"
-namespace fbf {
-
-#ifndef FBF_V2
-#define FBF_V2 0
+// The n = 0 term as a single-plane filter (fbf_capi.cu launch_fused_range).
+// At n = 0 the modulation is exact (c = 1, s = 0), so the harmonic's four
+// planes reduce to one: (q, p) = (conv(1), conv(f')) = (1, conv(f')) -- the
+// taps sum to one and mirror padding keeps it so (bilateral.hpp:126-144 with
+// n = 0).  Inside the fused kernel it would cost a full harmonic (four planes,
+// halo modulation, demodulation); here it is one separable FIR of f' read from
+// the padded (u, f') image, rounded to the same fixed-point grid as every other
+// term and written as group plane 0, onto which the fused kernel's group 0
+// accumulates harmonics 1..N.  The fixed-point sum is exact, so where the n = 0
+// term is computed does not change the result's bits.
+//
+// Tile: 64 output columns x 32 output rows per CTA (one tile per CTA), 256
+// threads.  smem: the (32+2W) x (64+2W) input tile of f' as row PAIRS (float2:
+// rows 2i, 2i+1), so the row pass filters two rows per FFMA2 with the tap as a
+// broadcast operand; the row-filtered (32+2W) x 64 tile is read as column
+// pairs by the column pass (FFMA2 again).
+constexpr int kN0TX = 64, kN0Threads = 256;
+template <int W, bool BOX, int TY>
+struct N0Cfg {
+  static constexpr int kN0TY = TY;
+  static constexpr int IW = kN0TX + 2 * W, IH = kN0TY + 2 * W;  // IH even
+  static constexpr int IWP = IW | 1;                            // pair-row pitch (float2 units)
+  static constexpr int RP = kN0TX + 2;                          // row-filtered pitch (floats, even)
+  static constexpr size_t smem_bytes = sizeof(float2) * size_t(IH / 2) * IWP + sizeof(float) * size_t(IH) * RP;
+  static constexpr int ROW_ITEMS = (IH / 2) * (kN0TX / 8);  // (row pair, 8 columns)
+  static constexpr int KC = 4;                              // column pass: (column pair, 4 rows)
+  static constexpr int COL_ITEMS = (kN0TX / 2) * (kN0TY / KC);
+};
+template <int W, bool BOX, int TY>
+#ifndef FBF_N0_MINB
+#define FBF_N0_MINB 1
 #endif
-// v2 schedule (fbf_fused2.cuh): small CTAs (two per SM) for W <= 9, big where
-// its tiles fit, else small with one CTA per SM
-template <int W, bool BOX>
-cudaError_t launch_w2(const FusedArgs& a, cudaStream_t st, int* grid_out) {
-  using Small = FusedCfg<W, 64, 16, 16, 16, 128, BOX>;
-  using Big = FusedCfg<W, 64, 32, 16, 16, 256, BOX>;
-  if constexpr (W <= 9 && V2<Small>::FITS2) {
-    return launch_cfg2<Small>(a, st, grid_out);
-  } else if constexpr (V2<Big>::FITS) {
-    return launch_cfg2<Big>(a, st, grid_out);
-  } else if constexpr (V2<Small>::FITS) {
-    return launch_cfg2<Small>(a, st, grid_out);
-  } else {
-    return cudaErrorInvalidValue;
+__global__ void __launch_bounds__(kN0Threads, FBF_N0_MINB) n0_plane_kernel(const __grid_constant__ FusedArgs A) {
+  using C = N0Cfg<W, BOX, TY>;
+  constexpr int kN0TY = TY;
+  extern __shared__ __align__(16) unsigned char n0s[];
+  p2* in2 = reinterpret_cast<p2*>(n0s);
+  float* rowt = reinterpret_cast<float*>(n0s + sizeof(float2) * size_t(C::IH / 2) * C::IWP);
+  const int pw = A.pq_cols + 2 * W, ph = A.g.out_rows + 2 * W;
+  const int tiles_x = A.pq_cols / kN0TX;
+  const int tiles_y = (A.g.out_rows + kN0TY - 1) / kN0TY;
+  const long long per_img = static_cast<long long>(tiles_x) * tiles_y;
+  const FixedScale fs = fixed_scale(A.h.aq, A.fmax);
+  const float d0 = A.h.d[0];
+  const p2 dd = pk(d0 * fs.sq, d0 * fs.sp);
+  auto tap = [&](int j) { return BOX ? A.k.box_tap : A.k.t[j < 0 ? -j : j]; };
+  const long long t = blockIdx.x;
+  const int b = static_cast<int>(t / per_img);
+  const int r = static_cast<int>(t - b * per_img);
+  const int ty = r / tiles_x, tx = r - ty * tiles_x;
+  const int x0 = tx * kN0TX, y0 = ty * kN0TY;  // padded coords of the tile's first input = output coords
+  const int2* __restrict__ img = A.uf + static_cast<long long>(b) * ph * pw;
+  float* in1 = reinterpret_cast<float*>(in2);
+  static_assert(C::IW % 2 == 0 && C::RP % 2 == 0, "pairs");
+  // load: warp = padded rows, lane = 16-byte column pairs (4 rows in flight)
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NP = C::IW / 2;  // IW even
+    constexpr int PER = (NP + 31) / 32;
+    for (int y4 = warp * 4; y4 < C::IH; y4 += 4 * (kN0Threads / 32)) {
+      int4 v[4][PER];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int py = min(y0 + min(y4 + r, C::IH - 1), ph - 1);  // past the image: clamped, never stored
+        const int4* __restrict__ row = reinterpret_cast<const int4*>(img + static_cast<long long>(py) * pw + x0);
+#pragma unroll
+        for (int c = 0; c < PER; ++c) v[r][c] = __ldg(row + min(lane + 32 * c, NP - 1));
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int yy = y4 + r;
+        if (yy < C::IH) {
+          float* dst = in1 + 2 * ((yy >> 1) * C::IWP) + (yy & 1);
+#pragma unroll
+          for (int c = 0; c < PER; ++c) {
+            const int xp = lane + 32 * c;
+            if (xp < NP) {
+              dst[2 * (2 * xp)] = __int_as_float(v[r][c].y);
+              dst[2 * (2 * xp + 1)] = __int_as_float(v[r][c].w);
+            }
+          }
+        }
+      }
+    }
   }
+  __syncthreads();
+  // row pass: item = (row pair, 8 output columns), FFMA2 over the pair; lanes
+  // walk pair rows (conflict-free LDS.64: odd pitch)
+  constexpr int NPR = C::IH / 2;
+  for (int it = threadIdx.x; it < C::ROW_ITEMS; it += kN0Threads) {
+    const int yp = it % NPR, xc = (it / NPR) * 8;
+    const p2* __restrict__ src = in2 + yp * C::IWP + xc;
+    p2 acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0ull;
+#pragma unroll
+    for (int m = 0; m < 8 + 2 * W; ++m) {
+      const p2 v = src[m];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int j = m - k;
+        if (j >= 0 && j <= 2 * W) {
+          const float tv = tap(j - W);
+          acc[k] = fma2(pk(tv, tv), v, acc[k]);
+        }
+      }
+    }
+    // (row 2yp, row 2yp+1) pairs -> column pairs of each row (8-byte stores)
+    p2* r0 = reinterpret_cast<p2*>(rowt + (2 * yp) * C::RP + xc);
+    p2* r1 = reinterpret_cast<p2*>(rowt + (2 * yp + 1) * C::RP + xc);
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+      float a0, a1, b0, b1;
+      upk(acc[k], a0, a1);
+      upk(acc[k + 1], b0, b1);
+      r0[k / 2] = pk(a0, b0);
+      r1[k / 2] = pk(a1, b1);
+    }
+  }
+  __syncthreads();
+  // column pass: item = (column pair, run of KC output rows), FFMA2 over the pair
+  Pair* __restrict__ out0 = A.pq + static_cast<long long>(b) * A.g.out_rows * A.pq_cols + x0;
+  for (int it = threadIdx.x; it < C::COL_ITEMS; it += kN0Threads) {
+    const int xp = it % (kN0TX / 2), run = it / (kN0TX / 2);
+    p2 acc[C::KC];
+#pragma unroll
+    for (int k = 0; k < C::KC; ++k) acc[k] = 0ull;
+    const float* __restrict__ col = rowt + run * C::KC * C::RP + 2 * xp;
+#pragma unroll
+    for (int m = 0; m < C::KC + 2 * W; ++m) {
+      const p2 v = *reinterpret_cast<const p2*>(col + m * C::RP);
+#pragma unroll
+      for (int k = 0; k < C::KC; ++k) {
+        const int j = m - k;
+        if (j >= 0 && j <= 2 * W) {
+          const float tv = tap(j - W);
+          acc[k] = fma2(pk(tv, tv), v, acc[k]);
+        }
+      }
+    }
+    Pair* __restrict__ out = out0 + 2 * xp;
+#pragma unroll
+    for (int k = 0; k < C::KC; ++k) {
+      const int y = y0 + run * C::KC + k;
+      if (y < A.g.out_rows) {
+        float c0, c1;
+        upk(acc[k], c0, c1);
+        float q0, p0, q1, p1;
+        upk(to_fixed(mul2(dd, pk(1.0f, c0))), q0, p0);
+        upk(to_fixed(mul2(dd, pk(1.0f, c1))), q1, p1);
+        *reinterpret_cast<float4*>(out + static_cast<long long>(y) * A.pq_cols) = make_float4(q0, p0, q1, p1);
+      }
+    }
+  }
+}
+
+template <int W, bool BOX, int TY>
+cudaError_t launch_n0_ty(const FusedArgs& a, cudaStream_t st) {
+  using C = N0Cfg<W, BOX, TY>;
+  static_assert(C::smem_bytes <= 227 * 1024, "n0 tile exceeds shared memory");
+  thread_local int dev_done = -1;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev_done != dev) {
+    e = cudaFuncSetAttribute(n0_plane_kernel<W, BOX, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(C::smem_bytes));
+    if (e != cudaSuccess) return e;
+    dev_done = dev;
+  }
+  const long long tiles = static_cast<long long>(a.strips) * ((a.g.out_rows + TY - 1) / TY) * a.g.batch;
+  if (tiles > 0x7fffffffLL) return cudaErrorInvalidValue;
+  n0_plane_kernel<W, BOX, TY><<<static_cast<unsigned>(tiles), kN0Threads, C::smem_bytes, st>>>(a);
+  return cudaGetLastError();
+}
+// 128-row tiles (row-pass halo overhead (128+2W)/128) where they still give a
+// few CTAs per SM, else 32-row tiles (small images)
+template <int W, bool BOX>
+cudaError_t launch_n0(const FusedArgs& a_in, cudaStream_t st) {
+  FusedArgs a = a_in;
+  a.strips = (a.g.width + kFusedTW - 1) / kFusedTW;
+  a.pq_cols = a.strips * kFusedTW;
+  const long long tiles64 = static_cast<long long>(a.strips) * ((a.g.out_rows + 63) / 64) * a.g.batch;
+  int ty = tiles64 >= 8 * 148 ? 128 : tiles64 >= 2 * 148 ? 64 : 32;
+#ifdef FBF_EXPERIMENTS
+  ty = static_cast<int>(FBF_TUNABLE(N0_TY, ty));
+#endif
+  if (ty >= 128) return launch_n0_ty<W, BOX, 128>(a, st);
+  if (ty >= 64) return launch_n0_ty<W, BOX, 64>(a, st);
+  return launch_n0_ty<W, BOX, 32>(a, st);
 }
 
 // Small (128 threads, G=16, two CTAs per SM) for W <= 9, big (256 threads,
 // G=32, one CTA per SM) otherwise -- measured, profiles/r01_cfg_compare.txt.
 // FBF_FUSED_CFG=small|big overrides where both fit (experiment build only).
-template <int W, bool BOX>
-cudaError_t launch_w1(const FusedArgs& a, cudaStream_t st, int* grid_out) {
+template <int W, bool BOX = false>
+cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
+  if (a.n0_only) return launch_n0<W, BOX>(a, st);
   using Small = FusedCfg<W, 64, 16, 16, 16, 128, BOX>;
   using Big = FusedCfg<W, 64, 32, 16, 16, 256, BOX>;
 #ifdef FBF_EXPERIMENTS
@@ -784,14 +953,6 @@ cudaError_t launch_w1(const FusedArgs& a, cudaStream_t st, int* grid_out) {
     (void)env;
     return cudaErrorInvalidValue;
   }
-}
-
-template <int W, bool BOX = false>
-cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
-  if constexpr (FBF_V2)
-    return launch_w2<W, BOX>(a, st, grid_out);
-  else
-    return launch_w1<W, BOX>(a, st, grid_out);
 }
 
 }  // namespace fbf

@@ -89,6 +89,8 @@ struct FusedArgs {
   int unit_cost;           // extra cost of one work unit (its 2W-row prologue + bootstrap) in output rows
   unsigned long long* prof;  // phase cycle counters (FBF_PHASE_PROF builds only), else null
   int accumulate;  // 1: the launch's first harmonic adds to the (Q, P) planes instead of initialising them
+  int n0_only;     // 1: launch_fused runs n0_plane_kernel (the n = 0 term) instead of the fused kernel
+  int acc_group0;  // 1: group 0 alone accumulates (onto the n = 0 plane of n0_plane_kernel)
   Harmonics h;     // last: the coefficient block is the large member
 };
 
