@@ -34,8 +34,8 @@ cudaError_t launch_fused(const FusedArgs& a_in, cudaStream_t st, int* grid_out) 
   FusedArgs a = a_in;
 #ifdef FBF_PHASE_PROF
   if (!g_prof) {
-    cudaMalloc(&g_prof, 32 * sizeof(unsigned long long));
-    cudaMemset(g_prof, 0, 32 * sizeof(unsigned long long));
+    cudaMalloc(&g_prof, (32 + 4 * 1024) * sizeof(unsigned long long));
+    cudaMemset(g_prof, 0, (32 + 4 * 1024) * sizeof(unsigned long long));
   }
   a.prof = g_prof;
 #endif
@@ -62,12 +62,13 @@ cudaError_t launch_fused(const FusedArgs& a_in, cudaStream_t st, int* grid_out) 
 }  // namespace fbf
 
 #ifdef FBF_PHASE_PROF
-// diagnostics: summed per-phase cycles of thread 0 of every CTA (see fbf_fused.cuh)
+// diagnostics: summed per-phase cycles of thread 0 of every CTA (see fbf_fused.cuh),
+// then 4 words per CTA (smid, start ns, end ns, steps); out32 holds 32 + 4096 words
 extern "C" int fbf_debug_phase_prof(unsigned long long* out32) {
   if (!fbf::g_prof) return -1;
   cudaDeviceSynchronize();
-  cudaMemcpy(out32, fbf::g_prof, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-  cudaMemset(fbf::g_prof, 0, 32 * sizeof(unsigned long long));
+  cudaMemcpy(out32, fbf::g_prof, (32 + 4 * 1024) * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaMemset(fbf::g_prof, 0, (32 + 4 * 1024) * sizeof(unsigned long long));
   return 0;
 }
 #endif

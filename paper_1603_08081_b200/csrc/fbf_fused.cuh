@@ -26,6 +26,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -80,10 +81,19 @@ struct FusedCfg {
   static constexpr size_t OFF_CS = OFF_R + 2 * size_t(RING) * RP * 8;
   static constexpr size_t OFF_BAR = up128(OFF_CS + size_t(CRING) * CP * 8);
   static constexpr size_t smem_bytes = OFF_BAR + 16;
-  static_assert(KR == KC && (KR == 16 || KR == 8), "one lane per (half, KR outputs)");
+  static_assert(KR == KC && KR == 16, "one lane per (half, 16 outputs)");
   // warps sharing one 16-column chunk: the row-pass producers and column-pass
   // consumers of that chunk's ring columns (the S2 hand-off group)
   static constexpr int CHUNK_WARPS = (NT / 32) / (TW / HALF);
+  // warp -> (row group | run, 16-column chunk): the warps of a chunk (its S2
+  // pair) are consecutive, so the two warps of an SMSP (w, w + 4) belong to
+  // different pairs and drift apart, overlapping each other's non-FMA phases
+  // (measured: pairing them on one SMSP, or mixing row groups on an SMSP, is
+  // 1-10 % slower; profiles/r02_notes.md)
+  static constexpr int NCH = TW / HALF;
+  static constexpr int NRG = G / HALF;
+  static __device__ __forceinline__ int rg_of(int warp) { return warp % NRG; }
+  static __device__ __forceinline__ int chunk_of(int warp) { return warp / NRG; }
   static_assert(G % HALF == 0 && TW % HALF == 0, "tiling");
   static_assert((G / HALF) * (TW / KR) * 32 == NT, "row pass: one (16 rows, chunk) item per warp");
   static_assert((TW / HALF) * (G / KC) * 32 == NT, "column pass: one (16 columns, run) item per warp");
@@ -305,8 +315,8 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restric
                                          const Pending<C>& pd) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int h = lane >> 4;
-  const int g = (lane & 15) + C::HALF * (warp % (C::G / C::HALF));
-  const int xc = (warp / (C::G / C::HALF)) * C::KR;
+  const int g = (lane & 15) + C::HALF * C::rg_of(warp);
+  const int xc = C::chunk_of(warp) * C::KR;
   // no early exit: rows past the step's end filter stale (finite) M rows and
   // only their stores are predicated, so every lane stays converged for the
   // deferred demodulation's shuffles interleaved below
@@ -384,8 +394,8 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
   const int h = lane >> 4;
   // warp -> (column chunk, run) as in the row pass's (chunk, row group): the
   // warps that row-passed a chunk's columns are the ones that read them here
-  const int x = (lane & 15) + C::HALF * (warp / (C::G / C::KC));
-  const int gi = (warp % (C::G / C::KC)) * C::KC;  // first output row of this lane, rel. to o
+  const int x = (lane & 15) + C::HALF * C::chunk_of(warp);
+  const int gi = C::rg_of(warp) * C::KC;  // first output row of this lane, rel. to o
   const int r0 = o + gi;
   const int gx = u.x0 + x;
   const int nr = min(C::KC, u.y1 - r0);  // <= 0: this lane only helps with the modulation
@@ -525,6 +535,11 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
   const FixedScale fs = fixed_scale(A.h.aq, A.fmax);
   PhaseClock clk;
   clk.start();
+#ifdef FBF_PHASE_PROF
+  unsigned long long t_cta0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_cta0));
+  unsigned cta_steps = 0;
+#endif
 
   // this CTA group's harmonics [nb, ne)
   const int span = A.n_hi - A.n_lo;
@@ -623,7 +638,7 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
           if constexpr (C::CHUNK_WARPS == 1)
             __syncwarp();
           else
-            asm volatile("bar.sync %0, %1;" ::"r"(1 + static_cast<int>(threadIdx.x >> 5) / C::CHUNK_WARPS),
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + C::chunk_of(static_cast<int>(threadIdx.x >> 5))),
                          "n"(32 * C::CHUNK_WARPS)
                          : "memory");
         } else {
@@ -648,15 +663,36 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
         // The (Q, P) rows stored this step (generic proxy: deferred finishes in
         // this step's row pass, immediate ones in its column pass) are read
         // back by a TMA load (async proxy) in the next harmonic: order them
-        // before the S1 barrier that precedes any such load.
+        // before the S1 barrier that precedes any such load.  (Once per
+        // harmonic would suffice, but measured slower: profiles/r02_notes.md.)
         fence_proxy_async_global();
         clk.step();
+#ifdef FBF_PHASE_PROF
+        ++cta_steps;
+#endif
         ++mk;
       }
     }
     pos += len;
   }
   clk.flush(A.prof);
+#ifdef FBF_PHASE_PROF
+  // per-CTA record after the 32 phase words: smid, start / end (globaltimer ns), steps
+  if (threadIdx.x == 0 && A.prof) {
+    const unsigned cta = blockIdx.y * gridDim.x + blockIdx.x;
+    if (cta < 1024) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      unsigned long long* rec = A.prof + 32 + 4 * cta;
+      rec[0] = smid;
+      rec[1] = t_cta0;
+      rec[2] = t1;
+      rec[3] = cta_steps;
+    }
+  }
+#endif
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
