@@ -48,10 +48,23 @@ namespace fbf {
 // shared-memory traffic of the two FIR passes by ~40% (the FIR loads were
 // half of all smem wavefronts; profiles/r01_notes.md).  The two halves of an
 // output meet in the demodulation through one shuffle (lane ^ 16).
-template <int W_, int TW_, int G_, int KR_, int KC_, int NT_, bool BOX_ = false>
+// QT: the running (Q, P) of a work unit lives in tensor memory across all its
+// harmonics (256-thread kernels, units <= 16 steps = 512 rows).  Each column-
+// pass lane's 8 output rows x (Q, P) of a step are 16 TMEM columns of its own
+// lane (tcgen05.ld / st 32x32b.x16: one instruction each); warps w and w+4
+// share a lane quarter and take TMEM columns [0, 256) and [256, 512).  No
+// (Q, P) tile in shared memory, no (Q, P) TMA per step; the global plane is
+// read only at a unit's first harmonic (the n = 0 plane, or a previous chained
+// launch) and written only at its last (partial sums).  The freed 16 KB pay
+// for a 64-row CS ring whose column-pass windows never wrap (W + G <= 64).
+template <int W_, int TW_, int G_, int KR_, int KC_, int NT_, bool BOX_ = false, bool QT_ = false>
 struct FusedCfg {
   static constexpr int W = W_, TW = TW_, G = G_, KR = KR_, KC = KC_, NT = NT_;
   static constexpr bool BOX = BOX_;
+  static constexpr bool QT = QT_;
+  static_assert(!QT || (NT == 256 && G == 32 && KC == 16), "TMEM (Q, P): 8 warps, 16 steps of 32 rows");
+  static constexpr bool CS64 = QT && W + G <= 64;
+  static constexpr int SEG = QT ? 15 * G : (1 << 30);  // longest unit (TMEM columns; step 15 = scratch)
   // deferred demodulation (Pending): measured gains on the 256-thread Gaussian
   // kernels only (c2 +0.9 %, c4 +3.6 %); the short running-sum row pass of the
   // box path cannot hide it (c3 -4.6 %) and the 128-thread kernels break even
@@ -59,7 +72,7 @@ struct FusedCfg {
   static constexpr int MW = TW + 2 * W;   // modulated row width
   static constexpr int MP = MW | 1;       // M plane pitch in 8-byte units (odd: conflict-free row walks)
   static constexpr int RING = 2 * W + G;  // R ring rows
-  static constexpr int CRING = W + G;     // CS ring rows
+  static constexpr int CRING = CS64 ? 64 : W + G;  // CS ring rows
   static constexpr int RP = TW + 1;       // R plane pitch in 8-byte units
   static constexpr int CP = TW + 1;       // CS pitch in 8-byte units
   static constexpr int PROLOGUE = (2 * W + G - 1) / G;  // steps that only row-pass
@@ -68,7 +81,7 @@ struct FusedCfg {
   static constexpr size_t up128(size_t v) { return (v + 127) & ~size_t(127); }
   static constexpr size_t OFF_STAGE = 0;
   static constexpr size_t OFF_PQ = up128(OFF_STAGE + size_t(G) * MW * 8);
-  static constexpr size_t OFF_M = up128(OFF_PQ + size_t(G) * TW * 8);  // planes A, B
+  static constexpr size_t OFF_M = up128(OFF_PQ + (QT ? 0 : size_t(G) * TW * 8));  // planes A, B
   static constexpr size_t M_BYTES = 2 * size_t(G) * MP * 8;
   static constexpr size_t bytes_with(int nmb) {
     return up128(OFF_M + nmb * M_BYTES + 2 * size_t(RING) * RP * 8 + size_t(CRING) * CP * 8) + 16;
@@ -99,6 +112,37 @@ struct FusedCfg {
   static_assert((TW / HALF) * (G / KC) * 32 == NT, "column pass: one (16 columns, run) item per warp");
   static constexpr bool FITS = smem_bytes <= 227 * 1024;  // launchable at all (one CTA per SM)
 };
+
+// tensor memory: 32x32b.x16 = 16 consecutive 32-bit columns of this thread's lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, p2 (&v)[8]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = pki(static_cast<int>(r[2 * k]), static_cast<int>(r[2 * k + 1]));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const p2 (&v)[8]) {
+  uint32_t r[16];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    float a, b;
+    upk(v[k], a, b);
+    r[2 * k] = __float_as_uint(a);
+    r[2 * k + 1] = __float_as_uint(b);
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // Geometry of one work unit and the rows of step s (same for every harmonic).
 struct Unit {
@@ -272,6 +316,11 @@ struct Pending {
   p2 dd;           // (d_n 2^aq, d_n 2^ap)
   p2* dst;         // (Q, P) of this lane's first output row; rows A.pq_cols apart
   int nh;          // rows this lane stores (<= 0: nothing pending)
+  // QT: sums go to TMEM (taddr, one tcgen05.st after the last finish) unless tg
+  p2 out[KH];
+  uint32_t taddr;
+  bool tg;    // this batch goes to the global plane (the unit's last harmonic)
+  bool live;  // warp-uniform: a TMEM batch is pending
   // output row k of this lane: (q, p) = own half + partner's half
   __device__ __forceinline__ p2 qp(int k, int h) const {
     const p2 send = h ? part[k] : part[KH + k];
@@ -280,10 +329,29 @@ struct Pending {
   }
   // (Q, P) += round(d_n (q, p)) on the fixed-point grid (exact integer sum)
   __device__ __forceinline__ p2 accumulate(int k, p2 qpk) const { return iadd2(pq[k], to_fixed(mul2(dd, qpk))); }
-  __device__ __forceinline__ void finish(int k, int h, int stride) const {
+  __device__ __forceinline__ void finish(int k, int h, int stride) {
     const p2 v = accumulate(k, qp(k, h));
-    if (k < nh) dst[k * stride] = v;
+    if constexpr (C::QT)
+      out[k] = v;
+    else if (k < nh)
+      dst[k * stride] = v;
   }
+  // QT: the batch's store after finish(0..KH-1): TMEM (all lanes of the warp),
+  // or the global plane at the unit's last harmonic
+  // (straight-line: the TMEM store always executes -- into the scratch
+  // columns of step 15 when no batch is pending -- so ptxas needs no
+  // collective wrapper around the .aligned instruction)
+  __device__ __forceinline__ void flush(int stride) {
+    if constexpr (C::QT) {
+      tmem_st16((live && !tg) ? taddr : scratch, out);
+      const bool g = live && tg;
+#pragma unroll
+      for (int k = 0; k < KH; ++k)
+        if (g && k < nh) dst[k * static_cast<long long>(stride)] = out[k];
+      live = false;
+    }
+  }
+  uint32_t scratch;  // QT: TMEM columns of step 15 (never a real step: units <= 15 steps)
 };
 
 // Order in which the column FIR visits its input rows: alternately from both
@@ -312,7 +380,7 @@ __host__ __device__ constexpr int fir_order(int q, int n, bool oi) {
 template <class C>
 __device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restrict__ M, p2* __restrict__ R,
                                          float* __restrict__ CS, int a, int rows, int base,
-                                         const Pending<C>& pd) {
+                                         Pending<C>& pd) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int h = lane >> 4;
   const int g = (lane & 15) + C::HALF * C::rg_of(warp);
@@ -331,7 +399,10 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restric
   };
   const int rel = a + g - base;
   const int slot = rel % C::RING;
-  float* __restrict__ csrow = CS + 2 * (rel % C::CRING) * C::CP + h;
+  // CS slot of input row rel: CS64 keys it on the output row (rel - W) mod 64,
+  // so the column pass's 16-row windows start on multiples of 16 and never wrap
+  const int cslot = C::CS64 ? ((rel + 64 - C::W) & 63) : rel % C::CRING;
+  float* __restrict__ csrow = CS + 2 * cslot * C::CP + h;
   p2 acc[C::KR];
   if constexpr (C::BOX) {
     // running sum over the window [i, i+2W] (unweighted)
@@ -378,6 +449,7 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restric
 #pragma unroll
     for (int i = 0; i < C::KR; ++i) dst[i] = acc[i];
   }
+  if constexpr (C::DEFER) pd.flush(A.pq_cols);  // QT: the deferred batch's store
 }
 
 // Column pass: warp = (16 columns, one KC-run of output rows); lane l filters
@@ -389,7 +461,7 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
                                          const float* __restrict__ CS, const p2* __restrict__ pqs,
                                          const Unit& u, int o, int base, int dn_idx, bool first, bool divide,
                                          bool defer, const ModNext<C>& next, PhaseClock& clk, Pending<C>& pd,
-                                         const FixedScale& fs) {
+                                         const FixedScale& fs, uint32_t tbase, bool seg_first, bool seg_last) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int h = lane >> 4;
   // warp -> (column chunk, run) as in the row pass's (chunk, row group): the
@@ -458,31 +530,58 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
   clk.mark(5);
   // (q, p) = c (Gc, Fc) + s (Gs, Fs)   [bilateral.hpp:138-144, real form]:
   // this lane's half of every row now; the halves meet in Pending::qp
-  const int cs0 = (r0 - base) % C::CRING;
+  if constexpr (C::CS64) {
+    const float* __restrict__ csw = CS + 2 * (((r0 - u.y0) & 63) * C::CP + x) + h;  // window start: a multiple of 16
 #pragma unroll
-  for (int i = 0; i < C::KC; ++i) {
-    int sc = cs0 + i;
-    sc = sc >= C::CRING ? sc - C::CRING : sc;
-    const float w = CS[2 * (sc * C::CP + x) + h];
-    pd.part[i] = mul2(pk(w, w), acc[i]);
+    for (int i = 0; i < C::KC; ++i) {
+      const float w = csw[2 * i * C::CP];
+      pd.part[i] = mul2(pk(w, w), acc[i]);
+    }
+  } else {
+    const int cs0 = (r0 - base) % C::CRING;
+#pragma unroll
+    for (int i = 0; i < C::KC; ++i) {
+      int sc = cs0 + i;
+      sc = sc >= C::CRING ? sc - C::CRING : sc;
+      const float w = CS[2 * (sc * C::CP + x) + h];
+      pd.part[i] = mul2(pk(w, w), acc[i]);
+    }
   }
-  const p2* __restrict__ pqin = pqs + (gi + h * KH) * C::TW + x;
-#pragma unroll
-  for (int k = 0; k < KH; ++k) pd.pq[k] = first ? 0ull : pqin[k * C::TW];
   const int rr = r0 + h * KH;  // first output row of this lane
   pd.nh = gx < A.g.width ? nr - h * KH : 0;  // rows of this lane (may be <= 0)
+  p2* const gdst = reinterpret_cast<p2*>(A.pq) +
+                   ((blockIdx.y * A.g.batch + u.b) * static_cast<long long>(A.g.out_rows) + (rr - A.g.out_row0)) *
+                       A.pq_cols +
+                   gx;
+  if constexpr (C::QT) {
+    // this lane's 16 TMEM columns of the step; (Q, P) from TMEM, or from the
+    // global plane at the unit's first harmonic when the launch accumulates
+    pd.taddr = tbase + 16u * static_cast<uint32_t>((o - u.y0) / C::G);
+    pd.scratch = tbase + 16u * 15u;
+    pd.tg = seg_last && !divide;
+    tmem_wait_st();
+    tmem_ld16(pd.taddr, pd.pq);  // unconditional (see flush); replaced below when not the running sum
+    if (first || seg_first) {
+#pragma unroll
+      for (int k = 0; k < KH; ++k)
+        pd.pq[k] = (!first && k < pd.nh) ? gdst[k * static_cast<long long>(A.pq_cols)] : 0ull;
+    }
+  } else {
+    const p2* __restrict__ pqin = pqs + (gi + h * KH) * C::TW + x;
+#pragma unroll
+    for (int k = 0; k < KH; ++k) pd.pq[k] = first ? 0ull : pqin[k * C::TW];
+  }
   // box: both passes summed unweighted; the weight (1/(2W+1))^2 = w0 joins d_n here
   // d_n (dn_idx = n - d_base: the launch's coefficient block)
   const float dn = C::BOX ? A.h.d[dn_idx] * (A.k.box_tap * A.k.box_tap) : A.h.d[dn_idx];
   pd.dd = pk(dn * fs.sq, dn * fs.sp);  // exact: powers of two
   if (!divide) {
-    pd.dst = reinterpret_cast<p2*>(A.pq) +
-             ((blockIdx.y * A.g.batch + u.b) * static_cast<long long>(A.g.out_rows) + (rr - A.g.out_row0)) *
-                 A.pq_cols +
-             gx;
+    pd.dst = gdst;
+    pd.live = true;
     if (!defer) {
 #pragma unroll
       for (int k = 0; k < KH; ++k) pd.finish(k, h, A.pq_cols);
+      pd.flush(A.pq_cols);
       pd.nh = 0;
     }
     return;
@@ -532,6 +631,8 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
   unsigned ph_uf = 0;  // phase parity of the next completion of the copy barrier
   Pending<C> pd;
   pd.nh = 0;
+  pd.live = false;
+  pd.tg = false;
   const FixedScale fs = fixed_scale(A.h.aq, A.fmax);
   PhaseClock clk;
   clk.start();
@@ -546,6 +647,24 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
   const int nb = A.n_lo + span * static_cast<int>(blockIdx.y) / A.groups;
   const int ne = A.n_lo + span * static_cast<int>(blockIdx.y + 1) / A.groups;
   if (nb >= ne) return;
+  // QT: warp 0 allocates all 512 TMEM columns (one CTA per SM); this thread's
+  // base: its warp's lane quarter, columns [0, 256) or [256, 512)
+  uint32_t tbase = 0;
+  if constexpr (C::QT) {
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + C::OFF_BAR + 8);
+    if (threadIdx.x < 32) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(tslot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int warp = static_cast<int>(threadIdx.x >> 5);
+    tbase = *tslot + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + 256u * static_cast<uint32_t>(warp >> 2);
+    pd.scratch = tbase + 16u * 15u;
+    pd.taddr = pd.scratch;
+  }
   // the harmonic whose (Q, P) initialises the planes (none for a chained launch
   // that accumulates onto an earlier one)
   const int n_first = (A.accumulate || (A.acc_group0 && blockIdx.y == 0)) ? -1 : nb;
@@ -578,7 +697,7 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
     const long long sidx = pos / A.g.out_rows;
     const int r0 = static_cast<int>(pos - sidx * A.g.out_rows);
     const int len = static_cast<int>(min(min(static_cast<long long>(A.g.out_rows - r0), hi - pos),
-                                         static_cast<long long>(A.seg_max)));
+                                         static_cast<long long>(min(A.seg_max, C::SEG))));
     Unit u;
     u.b = static_cast<int>(sidx / A.strips);
     u.x0 = static_cast<int>(sidx - static_cast<long long>(u.b) * A.strips) * C::TW;
@@ -607,7 +726,7 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
         step_rows<C>(u, s, a, rows, o);
         const bool wrap = s + 1 == nsteps;  // next step is step 0 of harmonic n+1
         const bool more = !wrap || n + 1 < ne;
-        const bool want_pq = o >= 0 && !first;
+        const bool want_pq = o >= 0 && !first && !C::QT;
         step_rows<C>(u, wrap ? 0 : s + 1, a2, rows2, o2);
         clk.mark(0);
         __syncthreads();  // S1: M holds this step; the previous column pass is done; stage free
@@ -654,7 +773,8 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
           // two steps (nsteps > 2; the generic-proxy stores keep the same
           // distance to the next harmonic's async-proxy (Q, P) load as before)
           const bool defer = C::DEFER && more && !divide && nsteps > 2;
-          col_pass<C>(A, R, CS, pqs, u, o, base, n - A.h.d_base, first, divide, defer, next, clk, pd, fs);
+          col_pass<C>(A, R, CS, pqs, u, o, base, n - A.h.d_base, first, divide, defer, next, clk, pd, fs, tbase,
+                      n == nb, n + 1 == ne);
           clk.mark(7);
         } else {
           modulate_rows<C>(stage, next.M, rows2, next.n);
@@ -674,6 +794,15 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
       }
     }
     pos += len;
+  }
+  if constexpr (C::QT) {  // every warp is done with its TMEM columns
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (threadIdx.x < 32) {
+      const uint32_t t0 = *reinterpret_cast<uint32_t*>(smem + C::OFF_BAR + 8);
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(t0) : "memory");
+    }
   }
   clk.flush(A.prof);
 #ifdef FBF_PHASE_PROF
@@ -967,11 +1096,31 @@ cudaError_t launch_n0(const FusedArgs& a_in, cudaStream_t st) {
 // Small (128 threads, G=16, two CTAs per SM) for W <= 9, big (256 threads,
 // G=32, one CTA per SM) otherwise -- measured, profiles/r01_cfg_compare.txt.
 // FBF_FUSED_CFG=small|big overrides where both fit (experiment build only).
+// TMEM (Q, P) when every CTA's rows fit one unit of <= 16 steps (no extra
+// prologues from the 512-row cap): small and medium images (c2), not the
+// long per-CTA runs of c4 / c5
+inline bool qt_fits(const FusedArgs& a, int groups, int seg_rows) {
+  thread_local int dev = -1, sms = 148;
+  int d = 0;
+  if (cudaGetDevice(&d) == cudaSuccess && d != dev) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+    dev = d;
+  }
+  const long long strips = (a.g.width + kFusedTW - 1) / kFusedTW;
+  const long long total = static_cast<long long>(a.g.batch) * strips * a.g.out_rows;
+  const long long ctas = std::max(1, sms / std::max(1, groups));
+  return (total + ctas - 1) / ctas + 32 <= seg_rows;
+}
+
 template <int W, bool BOX = false>
 cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
   if (a.n0_only) return launch_n0<W, BOX>(a, st);
   using Small = FusedCfg<W, 64, 16, 16, 16, 128, BOX>;
   using Big = FusedCfg<W, 64, 32, 16, 16, 256, BOX>;
+  using BigQ = FusedCfg<W, 64, 32, 16, 16, 256, BOX, true>;
+  if constexpr (!BOX && W > 9 && BigQ::FITS) {
+    if (FBF_TUNABLE(QT, 0) != 0 && qt_fits(a, std::max(1, a.groups), BigQ::SEG)) return launch_cfg<BigQ>(a, st, grid_out);
+  }
 #ifdef FBF_EXPERIMENTS
   const char* env = getenv("FBF_FUSED_CFG");
 #else
