@@ -1117,10 +1117,12 @@ cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
   if (a.n0_only) return launch_n0<W, BOX>(a, st);
   using Small = FusedCfg<W, 64, 16, 16, 16, 128, BOX>;
   using Big = FusedCfg<W, 64, 32, 16, 16, 256, BOX>;
+#ifdef FBF_EXPERIMENTS  // TMEM (Q, P): measured slower (profiles/r02_notes.md), experiment build only
   using BigQ = FusedCfg<W, 64, 32, 16, 16, 256, BOX, true>;
   if constexpr (!BOX && W > 9 && BigQ::FITS) {
     if (FBF_TUNABLE(QT, 0) != 0 && qt_fits(a, std::max(1, a.groups), BigQ::SEG)) return launch_cfg<BigQ>(a, st, grid_out);
   }
+#endif
 #ifdef FBF_EXPERIMENTS
   const char* env = getenv("FBF_FUSED_CFG");
 #else
