@@ -7,23 +7,27 @@ namespace fbf {
 
 #define FBF_EXTERN(WW, BB) extern template cudaError_t launch_w<WW, BB>(const FusedArgs&, cudaStream_t, int*);
 #define FBF_RADII(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) \
-  X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30)
+  X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32) X(33) \
+  X(34) X(35) X(36) X(37) X(38) X(39) X(40)
 #define FBF_EXTERN_G(WW) FBF_EXTERN(WW, false)
 FBF_RADII(FBF_EXTERN_G)
-#define FBF_BOX_RADII(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
+#define FBF_BOX_RADII(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) \
+  X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24)
 #define FBF_EXTERN_B(WW) FBF_EXTERN(WW, true)
 FBF_BOX_RADII(FBF_EXTERN_B)
 #undef FBF_EXTERN_G
 #undef FBF_EXTERN_B
 
-// Gaussian radii 1..30 (sigma <= 10) have a fused kernel -- make_spatial_gaussian
-// gives W = ceil(3 sigma), so the reference CLI's sweep (cli.hpp: sigma 1..12)
-// leaves only sigma 11 and 12 to the naive chain; box windows: radii 1..16
-// (c3 is 5; the CLI's box radius is ceil(sigma)), with running-sum passes.
-// Everything else takes the naive multi-kernel path.
+// Gaussian radii 1..40 (sigma <= 13.3) have a fused kernel -- make_spatial_gaussian
+// gives W = ceil(3 sigma), which covers the reference CLI's whole sweep
+// (cli.hpp:77, sigma 1..12 -> W <= 36); box windows: radii 1..24 (c3 is 5; the
+// CLI's box radius is ceil(sigma)), with running-sum passes.  Radii above 25
+// run the 128-thread tile with one CTA per SM (the 256-thread tiles exceed
+// shared memory).  Everything else takes the naive multi-kernel path (any
+// radius).
 bool fused_supported(int W, bool box) {
-  if (box) return W >= 1 && W <= 16;
-  return W >= 1 && W <= 30;
+  if (box) return W >= 1 && W <= 24;
+  return W >= 1 && W <= 40;
 }
 
 #ifdef FBF_PHASE_PROF

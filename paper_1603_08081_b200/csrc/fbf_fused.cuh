@@ -288,6 +288,24 @@ struct PhaseClock {
       for (int i = 0; i < 10; ++i) atomicAdd(out + (threadIdx.x ? 10 : 0) + i, ph[i]);
   }
   __device__ __forceinline__ void step() { ph[9] += on(); }
+#elif defined(FBF_SHAKE)
+  // race shaking (make shake): at every phase mark each warp sleeps a random
+  // 0-2 us with probability 3/8, so the warps' relative timing differs from
+  // run to run and from the product build; any missing barrier, fence or
+  // mbarrier phase shows up as results that are not bit-identical
+  // (tools/shake_check.py).  compute-sanitizer is not available on the GPU pool.
+  unsigned st;
+  __device__ __forceinline__ void start() {
+    st = static_cast<unsigned>(clock64()) * 2654435761u ^ (blockIdx.x * 40503u + blockIdx.y * 9973u) ^
+         ((threadIdx.x >> 5) * 0x9e3779b9u);
+  }
+  __device__ __forceinline__ void mark(int) {
+    st = st * 1664525u + 1013904223u;
+    const unsigned x = __shfl_sync(0xffffffffu, st, 0);
+    if ((x >> 29) < 3) __nanosleep((x >> 8) & 2047u);
+  }
+  __device__ __forceinline__ void step() {}
+  __device__ __forceinline__ void flush(unsigned long long*) {}
 #else
   __device__ __forceinline__ void step() {}
   __device__ __forceinline__ void start() {}

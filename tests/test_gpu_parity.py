@@ -101,9 +101,9 @@ def test_edge_shapes_all_radii(oracle, shape, sigma):
     assert maxabs(fb.bilateral_fast(img, s, a), oracle_rows(oracle, img, s, a, nthreads=1)) <= TOL
 
 
-@pytest.mark.parametrize("radius", [1, 2, 4, 7, 10, 16, 17])
+@pytest.mark.parametrize("radius", [1, 2, 4, 7, 10, 16, 17, 24, 25])
 def test_box_radii(oracle, radius):
-    """Box windows: running-sum fused instances for radii 1..16, the naive chain beyond."""
+    """Box windows: running-sum fused instances for radii 1..24, the naive chain beyond."""
     rng = np.random.default_rng(radius)
     img = rng.integers(0, 256, (37, 45)).astype(np.float64)
     s = fb.make_spatial_box(radius)
@@ -237,10 +237,11 @@ def test_exponential_kernel_high_order(oracle):
     assert maxabs(gpu, oracle_rows(oracle, img, s, a)) <= TOL
 
 
-@pytest.mark.parametrize("sigma", [0.3, 0.6, 1.3, 2.3, 3.3, 3.6, 4.3, 6.0, 7.0, 8.7, 10.0])
-def test_fused_radii_1_to_30(oracle, sigma):
-    """Every Gaussian radius 1..30 (sigma <= 10) has a fused instance; large
-    radii run one 128-thread CTA per SM (the 256-thread tiles exceed shared memory)."""
+@pytest.mark.parametrize("sigma", [0.3, 0.6, 1.3, 2.3, 3.3, 3.6, 4.3, 6.0, 7.0, 8.7, 10.0, 11.0, 12.0, 13.3])
+def test_fused_radii_1_to_40(oracle, sigma):
+    """Every Gaussian radius 1..40 (sigma <= 13.3, the reference CLI sweep's
+    sigma <= 12 included) has a fused instance; radii above 25 run one
+    128-thread CTA per SM (the 256-thread tiles exceed shared memory)."""
     rng = np.random.default_rng(int(sigma * 10))
     img = rng.integers(0, 256, (72, 130)).astype(np.float64)
     s = fb.make_spatial_gaussian(sigma)
