@@ -842,6 +842,8 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
 #endif
 }
 
+inline int groups_of(const FusedArgs& a) { return a.groups < 1 ? 1 : a.groups; }
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 inline cudaError_t encode_tile_3d(CUtensorMap* m, const void* base, unsigned long long d0,
                                   unsigned long long d1, unsigned long long d2, unsigned b0, unsigned b1) {
@@ -915,6 +917,28 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
   if (grid > by_work) grid = by_work;
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = static_cast<int>(grid);
+  // L2-resident units: every harmonic re-reads a unit's (u, f') tiles and
+  // read-modify-writes its (Q, P) rows.  When the CTAs' long runs (c5: 1,024-row
+  // images, 148 CTAs) make that working set exceed L2, it streams from HBM
+  // once per harmonic (c5: 128 GB per launch for 2.1 GB of image).  Capping a
+  // unit's rows so grid x ((rows + 2W)(TW + 2W) + rows TW) x 8 B fits in ~80 %
+  // of L2 keeps it resident, at the price of one more prologue per unit --
+  // taken only where that prologue costs < 3 % (c5 yes; c4's 48-row prologue
+  // no, measured -7 %).
+  if (a.seg_max >= (1 << 30)) {
+    const long long per_cta = a.total / std::max(1LL, grid);
+    for (int seg = 2048; seg >= 512; seg /= 2) {
+      const double ws = static_cast<double>(grid) * groups_of(a) *
+                        ((seg + 2.0 * C::W) * (C::TW + 2.0 * C::W) + seg * static_cast<double>(C::TW)) * 8.0;
+      if (per_cta > seg && ws <= 0.8 * 126e6 && kUnitCostFrac * 2.0 * C::W / seg <= 0.03) {
+        a.seg_max = seg;
+        break;
+      }
+    }
+  }
+#ifdef FBF_EXPERIMENTS
+  a.seg_max = static_cast<int>(FBF_TUNABLE(SEG_MAX, a.seg_max));
+#endif
   fused_kernel<C><<<dim3(static_cast<unsigned>(grid), static_cast<unsigned>(a.groups)), C::NT, C::smem_bytes, st>>>(a);
   return cudaGetLastError();
 }
