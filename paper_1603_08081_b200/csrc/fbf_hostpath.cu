@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <condition_variable>
 #include <cstdio>
@@ -165,6 +166,11 @@ int host_ctx(size_t bytes, HostCtx*& out) {
 
 // A persistent pool for the host-side double <-> float conversions of the f64
 // entry points (one process-wide pool; concurrent callers take turns).
+// Dispatch is a generation counter: workers spin on it for a while after each
+// job before sleeping on the condition variable, and the caller spins on the
+// pending count -- a call's successive conversions (and back-to-back calls)
+// then start in ~1 us instead of a futex wake-up of every worker per
+// conversion, which dominated small calls (c1 e2e_f64, profiles/r02_notes.md).
 class Pool {
  public:
   static Pool& get() {
@@ -176,22 +182,22 @@ class Pool {
   void run(const std::function<void(int, int)>& fn) {
     std::lock_guard<std::mutex> call(call_);
     const int parts = size();
+    job_ = &fn;
+    pending_.store(parts - 1, std::memory_order_relaxed);
     {
       std::lock_guard<std::mutex> lk(m_);
-      job_ = &fn;
-      pending_ = parts - 1;
-      ++gen_;
+      gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     fn(0, parts);
-    std::unique_lock<std::mutex> lk(m_);
-    done_.wait(lk, [&] { return pending_ == 0; });
+    while (pending_.load(std::memory_order_acquire) != 0) std::this_thread::yield();
     job_ = nullptr;
   }
   ~Pool() {
     {
       std::lock_guard<std::mutex> lk(m_);
-      stop_ = true;
+      stop_.store(true);
+      gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     for (auto& t : workers_) t.join();
@@ -206,26 +212,29 @@ class Pool {
   void loop(int part) {
     unsigned long long seen = 0;
     for (;;) {
-      const std::function<void(int, int)>* job;
-      {
-        std::unique_lock<std::mutex> lk(m_);
-        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
-        if (stop_) return;
-        seen = gen_;
-        job = job_;
+      // spin ~2 ms on the generation counter, then sleep
+      const auto t0 = std::chrono::steady_clock::now();
+      int it = 0;
+      while (gen_.load(std::memory_order_acquire) == seen) {
+        if ((++it & 255) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2)) {
+          std::unique_lock<std::mutex> lk(m_);
+          cv_.wait(lk, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+          break;
+        }
       }
-      (*job)(part, static_cast<int>(workers_.size()) + 1);
-      std::lock_guard<std::mutex> lk(m_);
-      if (--pending_ == 0) done_.notify_one();
+      seen = gen_.load(std::memory_order_acquire);
+      if (stop_.load()) return;
+      (*job_)(part, static_cast<int>(workers_.size()) + 1);
+      pending_.fetch_sub(1, std::memory_order_acq_rel);
     }
   }
   std::vector<std::thread> workers_;
   std::mutex call_, m_;
-  std::condition_variable cv_, done_;
+  std::condition_variable cv_;
   const std::function<void(int, int)>* job_ = nullptr;
-  int pending_ = 0;
-  unsigned long long gen_ = 0;
-  bool stop_ = false;
+  std::atomic<int> pending_{0};
+  std::atomic<unsigned long long> gen_{0};
+  std::atomic<bool> stop_{false};
 };
 
 // rows [r0, r1) of each image b in [b0, b1): out (dense, pitch w) <- in (strided)
