@@ -64,6 +64,15 @@ struct FusedCfg {
   static constexpr bool QT = QT_;
   static_assert(!QT || (NT == 256 && G == 32 && KC == 16), "TMEM (Q, P): 8 warps, 16 steps of 32 rows");
   static constexpr bool CS64 = QT && W + G <= 64;
+  // PQG: the running (Q, P) rows are loaded by their own column-pass lane from
+  // global memory (L2; written by the same lane in the previous harmonic:
+  // program order, no proxy fence) instead of a per-step TMA tile in shared
+  // memory -- 16 KB freed (for the column-major R ring), no (Q, P) TMA on the
+  // leader's critical path
+#ifndef FBF_PQLDG
+#define FBF_PQLDG 0
+#endif
+  static constexpr bool PQG = FBF_PQLDG != 0 && !QT;
   static constexpr int SEG = QT ? 15 * G : (1 << 30);  // longest unit (TMEM columns; step 15 = scratch)
   // deferred demodulation (Pending): measured gains on the 256-thread Gaussian
   // kernels only (c2 +0.9 %, c4 +3.6 %); the short running-sum row pass of the
@@ -73,7 +82,21 @@ struct FusedCfg {
   static constexpr int MP = MW | 1;       // M plane pitch in 8-byte units (odd: conflict-free row walks)
   static constexpr int RING = 2 * W + G;  // R ring rows
   static constexpr int CRING = CS64 ? 64 : W + G;  // CS ring rows
-  static constexpr int RP = TW + 1;       // R plane pitch in 8-byte units
+  static constexpr int RP = TW + 1;       // R plane pitch in 8-byte units (row-major R)
+  // Column-major R (RCOL): plane h, column x, ring slot: (h TW + x) RPT + slot,
+  // RPT = RING rounded up to 2 mod 4 (a 2 RPT-word stride = 4 mod 8: the
+  // 16-byte loads of 8 consecutive columns hit 8 distinct bank quads).  A column-pass lane then loads two consecutive ring
+  // rows with one LDS.128 (slot and RING are even: a pair never straddles the
+  // wrap), halving its ring loads and their wrap arithmetic.
+#ifndef FBF_RCOL
+#define FBF_RCOL 1
+#endif
+  // (the 256-thread Gaussian kernels: measured c2 +1.3 %, c5 +1.5 %, c4 +2.1 %;
+  // the box path's single-row running-sum loads conflict in this layout, c3 -11 %;
+  // the 128-thread W <= 9 kernel breaks even)
+  static constexpr bool RCOL = FBF_RCOL != 0 && !BOX && NT > 128;
+  static constexpr int RPT = RING % 4 == 2 ? RING : RING + 2;
+  static constexpr size_t R_BYTES = RCOL ? 2 * size_t(TW) * RPT * 8 : 2 * size_t(RING) * RP * 8;
   static constexpr int CP = TW + 1;       // CS pitch in 8-byte units
   static constexpr int PROLOGUE = (2 * W + G - 1) / G;  // steps that only row-pass
   static constexpr int HALF = 16;         // lanes per channel half
@@ -81,17 +104,17 @@ struct FusedCfg {
   static constexpr size_t up128(size_t v) { return (v + 127) & ~size_t(127); }
   static constexpr size_t OFF_STAGE = 0;
   static constexpr size_t OFF_PQ = up128(OFF_STAGE + size_t(G) * MW * 8);
-  static constexpr size_t OFF_M = up128(OFF_PQ + (QT ? 0 : size_t(G) * TW * 8));  // planes A, B
+  static constexpr size_t OFF_M = up128(OFF_PQ + (QT || PQG ? 0 : size_t(G) * TW * 8));  // planes A, B
   static constexpr size_t M_BYTES = 2 * size_t(G) * MP * 8;
   static constexpr size_t bytes_with(int nmb) {
-    return up128(OFF_M + nmb * M_BYTES + 2 * size_t(RING) * RP * 8 + size_t(CRING) * CP * 8) + 16;
+    return up128(OFF_M + nmb * M_BYTES + R_BYTES + size_t(CRING) * CP * 8) + 16;
   }
   // M double-buffered where it fits: the next step's modulation then writes the
   // other buffer, and the row pass -> column pass hand-off only syncs the two
   // warps of a column chunk (their rows and columns) instead of the whole CTA
   static constexpr int NMB = NT > 128 && bytes_with(2) <= 227 * 1024 ? 2 : 1;  // small CTAs: keep 2 per SM
   static constexpr size_t OFF_R = OFF_M + NMB * M_BYTES;  // planes A, B
-  static constexpr size_t OFF_CS = OFF_R + 2 * size_t(RING) * RP * 8;
+  static constexpr size_t OFF_CS = OFF_R + R_BYTES;
   static constexpr size_t OFF_BAR = up128(OFF_CS + size_t(CRING) * CP * 8);
   static constexpr size_t smem_bytes = OFF_BAR + 16;
   static_assert(KR == KC && KR == 16, "one lane per (half, 16 outputs)");
@@ -463,9 +486,15 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restric
     }
   }
   if (live) {
-    p2* __restrict__ dst = R + (h * C::RING + slot) * C::RP + xc;
+    if constexpr (C::RCOL) {
+      p2* __restrict__ dst = R + (h * C::TW + xc) * C::RPT + slot;
 #pragma unroll
-    for (int i = 0; i < C::KR; ++i) dst[i] = acc[i];
+      for (int i = 0; i < C::KR; ++i) dst[i * C::RPT] = acc[i];
+    } else {
+      p2* __restrict__ dst = R + (h * C::RING + slot) * C::RP + xc;
+#pragma unroll
+      for (int i = 0; i < C::KR; ++i) dst[i] = acc[i];
+    }
   }
   if constexpr (C::DEFER) pd.flush(A.pq_cols);  // QT: the deferred batch's store
 }
@@ -491,7 +520,16 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
   const int nr = min(C::KC, u.y1 - r0);  // <= 0: this lane only helps with the modulation
   p2 acc[C::KC];
   constexpr int KH = C::KC / 2;
-  const p2* __restrict__ Rh = R + h * C::RING * C::RP + x;
+  if constexpr (C::PQG) {  // the lane's running (Q, P) rows: issued now, used after the FIR
+    const int nh0 = gx < A.g.width ? nr - h * KH : 0;
+    const p2* gq = reinterpret_cast<const p2*>(A.pq) +
+                   ((blockIdx.y * A.g.batch + u.b) * static_cast<long long>(A.g.out_rows) +
+                    (r0 + h * KH - A.g.out_row0)) * A.pq_cols + gx;
+#pragma unroll
+    for (int k = 0; k < KH; ++k)
+      pd.pq[k] = (first || k >= nh0) ? 0ull : gq[k * static_cast<long long>(A.pq_cols)];
+  }
+  const p2* __restrict__ Rh = C::RCOL ? R + (h * C::TW + x) * C::RPT : R + h * C::RING * C::RP + x;
   const int s0 = (r0 - C::W - base) % C::RING;
   constexpr int TAPS_IN = C::KC + 2 * C::W;
   constexpr int NBATCH = ModNext<C>::NBATCH;
@@ -508,7 +546,15 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
   auto ring = [&](int m) {
     int s = s0 + m;
     s = s >= C::RING ? s - C::RING : s;
-    return Rh[s * C::RP];
+    return Rh[s * (C::RCOL ? 1 : C::RP)];
+  };
+  // rows m, m + 1 (m even) in one 16-byte load (RCOL)
+  auto ring2 = [&](int m, p2& v0, p2& v1) {
+    int s = s0 + m;
+    s = s >= C::RING ? s - C::RING : s;
+    const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(Rh + s);
+    v0 = t.x;
+    v1 = t.y;
   };
   if constexpr (C::BOX) {
     p2 sum = 0ull;
@@ -527,10 +573,7 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
   } else {
 #pragma unroll
     for (int i = 0; i < C::KC; ++i) acc[i] = 0ull;
-#pragma unroll
-    for (int q = 0; q < TAPS_IN; ++q) {
-      const int m = fir_order(q, TAPS_IN, FBF_FIR_OI_COL);
-      const p2 v = ring(m);
+    auto taps = [&](int m, p2 v) {
 #pragma unroll
       for (int i = 0; i < C::KC; ++i) {
         const int j = m - i;
@@ -539,7 +582,27 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
           acc[i] = fma2(pk(tv, tv), v, acc[i]);
         }
       }
-      batch(q);
+    };
+    if constexpr (C::RCOL) {
+      static_assert(TAPS_IN % 2 == 0 && C::RING % 2 == 0, "row pairs");
+      // pairs of input rows, visited outside-in like single rows below
+#pragma unroll
+      for (int qq = 0; qq < TAPS_IN / 2; ++qq) {
+        const int m = 2 * fir_order(qq, TAPS_IN / 2, FBF_FIR_OI_COL);
+        p2 v0, v1;
+        ring2(m, v0, v1);
+        taps(m, v0);
+        batch(2 * qq);
+        taps(m + 1, v1);
+        batch(2 * qq + 1);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < TAPS_IN; ++q) {
+        const int m = fir_order(q, TAPS_IN, FBF_FIR_OI_COL);
+        taps(m, ring(m));
+        batch(q);
+      }
     }
   }
 #pragma unroll
@@ -584,6 +647,8 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
       for (int k = 0; k < KH; ++k)
         pd.pq[k] = (!first && k < pd.nh) ? gdst[k * static_cast<long long>(A.pq_cols)] : 0ull;
     }
+  } else if constexpr (C::PQG) {
+    // (loaded at the head of the pass, in flight during the FIR)
   } else {
     const p2* __restrict__ pqin = pqs + (gi + h * KH) * C::TW + x;
 #pragma unroll
@@ -744,7 +809,7 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
         step_rows<C>(u, s, a, rows, o);
         const bool wrap = s + 1 == nsteps;  // next step is step 0 of harmonic n+1
         const bool more = !wrap || n + 1 < ne;
-        const bool want_pq = o >= 0 && !first && !C::QT;
+        const bool want_pq = o >= 0 && !first && !C::QT && !C::PQG;
         step_rows<C>(u, wrap ? 0 : s + 1, a2, rows2, o2);
         clk.mark(0);
         __syncthreads();  // S1: M holds this step; the previous column pass is done; stage free
@@ -803,7 +868,7 @@ __global__ void __launch_bounds__(C::NT, (C::NT <= 128 ? 2 : 1)) fused_kernel(co
         // back by a TMA load (async proxy) in the next harmonic: order them
         // before the S1 barrier that precedes any such load.  (Once per
         // harmonic would suffice, but measured slower: profiles/r02_notes.md.)
-        fence_proxy_async_global();
+        if constexpr (!C::PQG) fence_proxy_async_global();
         clk.step();
 #ifdef FBF_PHASE_PROF
         ++cta_steps;
