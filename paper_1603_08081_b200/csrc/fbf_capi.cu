@@ -21,7 +21,7 @@
 
 namespace fbf {
 bool fused_supported(int W, bool box);
-cudaError_t launch_fused(const FusedArgs& a, cudaStream_t st, int* grid_out);
+cudaError_t launch_fused(const FusedArgs& a, cudaStream_t st, FusedPlan* plan);
 }  // namespace fbf
 
 using namespace fbf;
@@ -281,42 +281,97 @@ __global__ void finish_kernel(const p2* __restrict__ pq, const double2* __restri
 // Sums the nonempty groups' fixed-point planes (exact integer adds: the
 // result does not depend on the group count) and divides, or writes the exact
 // fp64 (Q, P) values (sum_out, fbf_partial_sums_device).
-// Grid: x = column blocks, y = (image, output row) in a grid-stride loop.
-__global__ void finish_groups(const p2* __restrict__ pq, int groups, int span, long long plane, int pq_cols,
-                              Geometry g, float shift, float q_floor, unsigned long long* bad,
-                              float* __restrict__ dst, double2* __restrict__ sum_out, int aq,
-                              const unsigned* __restrict__ fmax) {
+// A thread takes PX adjacent pixels (PX = 2: one 16-byte load per plane; the
+// fused layout's even pitch) of kFinishRows consecutive rows, every load of
+// every plane issued before the first use (the pass is pure memory traffic:
+// one pixel per thread with 8-byte loads ran at ~1.5 TB/s, c2 with 2 groups
+// 48 us; this form ~3x faster).  Grid: x = column blocks, y = row groups in a
+// grid-stride loop.
+constexpr int kFinishRows = 4;
+constexpr int kFinishThreads = 128;
+template <int PX>
+__global__ void __launch_bounds__(kFinishThreads)
+    finish_groups(const p2* __restrict__ pq, int groups, int span, long long plane, int pq_cols, Geometry g,
+                  float shift, float q_floor, unsigned long long* bad, float* __restrict__ dst,
+                  double2* __restrict__ sum_out, int aq, const unsigned* __restrict__ fmax) {
   const FixedScale fs = fixed_scale(aq, fmax);
   const long long nrows = static_cast<long long>(g.out_rows) * g.batch;
-  for (long long row = blockIdx.y; row < nrows; row += gridDim.y) {
-    const int b = static_cast<int>(row / g.out_rows);
-    const int yl = static_cast<int>(row - static_cast<long long>(b) * g.out_rows);
-    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < g.width; x += gridDim.x * blockDim.x) {
-      const long long at = row * pq_cols + x;
-      p2 acc = 0ull;
-      for (int k = 0; k < groups; ++k)
-        if (span * (k + 1) / groups > span * k / groups) acc = iadd2(acc, pq[k * plane + at]);
-      if (sum_out) {  // exact: int32 * 2^-a is representable in fp64
-        float a, c;
-        upk(acc, a, c);
-        sum_out[row * g.width + x] = make_double2(static_cast<double>(__float_as_int(a)) * fs.iq,
-                                                  static_cast<double>(__float_as_int(c)) * fs.ip);
-        continue;
+  unsigned live = 0;  // groups that hold at least one harmonic (the others' planes were never written)
+  for (int k = 0; k < groups; ++k)
+    if (span * (k + 1) / groups > span * k / groups) live |= 1u << k;
+  for (long long row0 = static_cast<long long>(blockIdx.y) * kFinishRows; row0 < nrows;
+       row0 += static_cast<long long>(gridDim.y) * kFinishRows) {
+    for (int x = PX * (blockIdx.x * blockDim.x + threadIdx.x); x < g.width; x += PX * gridDim.x * blockDim.x) {
+      p2 acc[kFinishRows][PX];
+#pragma unroll
+      for (int r = 0; r < kFinishRows; ++r)
+#pragma unroll
+        for (int j = 0; j < PX; ++j) acc[r][j] = 0ull;
+      for (int k = 0; k < groups; ++k) {
+        if (!((live >> k) & 1u)) continue;
+        p2 v[kFinishRows][PX];
+#pragma unroll
+        for (int r = 0; r < kFinishRows; ++r) {
+          const long long row = min(row0 + r, nrows - 1);
+          const p2* src = pq + k * plane + row * pq_cols + x;
+          if constexpr (PX == 2) {
+            const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(src);
+            v[r][0] = t.x;
+            v[r][1] = t.y;
+          } else {
+            v[r][0] = *src;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < kFinishRows; ++r)
+#pragma unroll
+          for (int j = 0; j < PX; ++j) acc[r][j] = iadd2(acc[r][j], v[r][j]);
       }
-      float Q, P;
-      from_fixed(acc, fs, Q, P);
-      if (!(fabsf(Q) >= q_floor) && bad) {
-        const unsigned long long lin = static_cast<unsigned long long>(b) * g.full_height * g.width +
-                                       static_cast<unsigned long long>(g.out_row0 + yl) * g.width + x;
-        atomicMin(bad, lin);
+#pragma unroll
+      for (int r = 0; r < kFinishRows; ++r) {
+        const long long row = row0 + r;
+        if (row >= nrows) break;
+        const int b = static_cast<int>(row / g.out_rows);
+        const int yl = static_cast<int>(row - static_cast<long long>(b) * g.out_rows);
+#pragma unroll
+        for (int j = 0; j < PX; ++j) {
+          if (x + j >= g.width) break;
+          if (sum_out) {  // exact: int32 * 2^-a is representable in fp64
+            float a, c;
+            upk(acc[r][j], a, c);
+            sum_out[row * g.width + x + j] = make_double2(static_cast<double>(__float_as_int(a)) * fs.iq,
+                                                          static_cast<double>(__float_as_int(c)) * fs.ip);
+            continue;
+          }
+          float Q, P;
+          from_fixed(acc[r][j], fs, Q, P);
+          if (!(fabsf(Q) >= q_floor) && bad) {
+            const unsigned long long lin = static_cast<unsigned long long>(b) * g.full_height * g.width +
+                                           static_cast<unsigned long long>(g.out_row0 + yl) * g.width + x + j;
+            atomicMin(bad, lin);
+          }
+          dst[b * g.dst_bstride + static_cast<long long>(yl) * g.dst_pitch + x + j] = shift + __fdiv_rn(P, Q);
+        }
       }
-      dst[b * g.dst_bstride + static_cast<long long>(yl) * g.dst_pitch + x] = shift + __fdiv_rn(P, Q);
     }
   }
 }
-dim3 rows_grid(const Geometry& g) {
-  const long long rows = static_cast<long long>(g.out_rows) * g.batch;
-  return dim3(static_cast<unsigned>((g.width + 255) / 256), static_cast<unsigned>(std::min(rows, 65535LL)), 1);
+// pixel pairs where every plane row starts 16-byte aligned (the fused layout), else single pixels
+void launch_finish_groups(cudaStream_t st, const p2* pq, int groups, int span, long long plane, int pq_cols,
+                          const Geometry& g, float shift, float q_floor, unsigned long long* bad, float* dst,
+                          double2* sum_out, int aq, const unsigned* fmax) {
+  const long long nrows = static_cast<long long>(g.out_rows) * g.batch;
+  const unsigned gy = static_cast<unsigned>(std::min((nrows + kFinishRows - 1) / kFinishRows, 65535LL));
+  const bool pairs = pq_cols % 2 == 0 && plane % 2 == 0 && reinterpret_cast<uintptr_t>(pq) % 16 == 0;
+  if (pairs) {
+    const dim3 grid(static_cast<unsigned>((g.width + 2 * kFinishThreads - 1) / (2 * kFinishThreads)), gy, 1);
+    finish_groups<2><<<grid, kFinishThreads, 0, st>>>(pq, groups, span, plane, pq_cols, g, shift, q_floor, bad, dst,
+                                                      sum_out, aq, fmax);
+  } else {
+    const dim3 grid(static_cast<unsigned>((g.width + kFinishThreads - 1) / kFinishThreads), gy, 1);
+    finish_groups<1><<<grid, kFinishThreads, 0, st>>>(pq, groups, span, plane, pq_cols, g, shift, q_floor, bad, dst,
+                                                      sum_out, aq, fmax);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -500,59 +555,143 @@ void fill_harmonics(Harmonics& h, const fbf_filter* f) {
 // ---------------------------------------------------------------------------
 // Harmonic split inside one GPU: the harmonics are divided among CTA groups,
 // each accumulating its own fixed-point (Q, P) plane, summed exactly at the
-// end.  Each group's CTAs get work units with `groups` times more rows and
-// 1/groups of the harmonics, which cuts the per-harmonic 2W-row unit
-// prologues; large images lose to the extra planes and the finish pass.  The
-// count comes from a cost model (group_model) of the call's own output rows
-// and harmonic count.  Since the sums are integers, any count gives the same
-// bits.  Measured: profiles/r01_groups.txt, r01_notes.md.
+// end (finish_groups).  Each group's CTAs get work units with `groups` times
+// more rows and 1/groups of the harmonics: fewer per-harmonic 2W-row unit
+// prologues and a finer step granularity (a CTA's rows per harmonic are a
+// whole number of G-row steps: c2 with one group runs 16 steps on its busiest
+// CTAs against a mean of 15.1, with two groups 30 against 29.2), against the
+// extra planes and the finish pass.  Since the sums are integers, any count
+// gives the same bits; the count is purely a speed choice.
+//
+// Cost model (microseconds): for k groups the fused kernel's duration is
+// ceil(H / k) harmonics x the busiest CTA's steps per harmonic x the step
+// time.  The busiest CTA comes from replaying the kernel's own cuts
+// (fused_kernel: cost-balanced ranges in (strip, row) space, KC-aligned, units
+// capped at seg_max) on the launch plan of this geometry (launch_fused in
+// plan mode); a unit's prologue steps count 0.8 of a full step (c2: one group
+// 995 us, two groups 946 us, i.e. 15.6 against 29.6 / 2 steps per harmonic).
+// Step time: per pixel and harmonic on one SM, linear in the taps (fitted to
+// c5 / c2 / c4 at W = 12 / 15 / 24).  The finish pass moves 8 k + 4 bytes per
+// pixel at ~4 TB/s plus ~6 us.  Measured: profiles/r02_notes.md (groups).
+constexpr double kModelPrologueStep = 0.8;
+struct GroupCosts {
+  double per_harmonic[9] = {};  // [k]: busiest CTA's time for one harmonic, us
+  double finish[9] = {};        // [k]: finish_groups, us
+  bool ok = false;
+};
 
-// Cost model, in CTA rows of one harmonic: a CTA of group count k filters
-// ceil(H / k) harmonics over R / floor(ctas / k) rows, each harmonic paying
-// its unit's prologue (~0.55 * 2W rows, the fused kernel's unit cost).  A
-// larger k must win by 3 %: the extra planes and the finish pass are not in
-// the model (measured: c1 13 harmonics -> 7 groups, c3 31 -> 4, c2 21 -> 1).
-int group_model(const fbf_geometry* g, int radius, int H) {
-  int dev = 0, sms = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess) sm_count(dev, &sms);
-  const int ctas = sms * (radius <= 9 ? 2 : 1);  // launch_w: small CTAs for W <= 9
-  const double strips = std::ceil(g->width / static_cast<double>(kFusedTW));
-  const double rows = static_cast<double>(g->out_rows) * g->batch * strips;
-  const double u = 2.0 * radius * FBF_TUNABLE(UNIT_COST_FRAC, kUnitCostFrac);
+double busiest_cta_steps(const FusedPlan& p, const fbf_geometry* g) {
+  const long long strips = (g->width + p.tw - 1) / p.tw;
+  const long long out_rows = g->out_rows;
+  const long long total = static_cast<long long>(g->batch) * strips * out_rows;
+  const long long per = out_rows + p.unit_cost;
+  const long long ctotal = total / out_rows * per;
+  auto split = [&](long long pos) {
+    const long long sidx = pos / out_rows;
+    const long long r = pos - sidx * out_rows;
+    return sidx * out_rows + (r - r % p.kc);
+  };
+  auto cut = [&](long long k) {
+    const long long t = ctotal * k / p.grid;
+    const long long sidx = t / per;
+    return split(sidx * out_rows + std::min(t - sidx * per, out_rows));
+  };
+  double worst = 0.0;
+  long long lo = 0;
+  for (int b = 0; b < p.grid; ++b) {
+    const long long hi = b + 1 == p.grid ? total : cut(b + 1);
+    double steps = 0.0;
+    for (long long pos = lo; pos < hi;) {
+      const long long sidx = pos / out_rows;
+      const long long r0 = pos - sidx * out_rows;
+      const long long len = std::min({out_rows - r0, hi - pos, static_cast<long long>(p.seg_max)});
+      steps += kModelPrologueStep * p.prologue + static_cast<double>((len + p.G - 1) / p.G);
+      pos += len;
+    }
+    worst = std::max(worst, steps);
+    lo = hi;
+  }
+  return worst;
+}
+
+GroupCosts group_costs_of(const fbf_geometry* g, int radius, bool box) {
+  GroupCosts c;
+  if (!fused_supported(radius, box)) return c;
+  FusedArgs A;
+  std::memset(&A, 0, sizeof(A));
+  A.g = to_geometry(g);
+  A.k.W = radius;
+  A.k.box = box;
+  A.seg_max = 1 << 30;
+  const double px = static_cast<double>(g->batch) * g->out_rows * g->width;
+  for (int k = 1; k <= 8; ++k) {
+    A.groups = k;
+    FusedPlan p{};
+    if (launch_fused(A, nullptr, &p) != cudaSuccess || p.grid < 1) return c;  // no device: one group
+    const int conc = std::max(1, std::min(p.occ, (p.grid * k + p.sms - 1) / p.sms));  // CTAs sharing an SM
+    double t_px = box ? 0.70e-3 * (kFusedTW + 2.0 * radius) / 74.0
+                      : (0.86 + 0.0757 * (2.0 * radius + 1.0)) / 2048.0;  // us per pixel and harmonic on one SM
+    if (p.nt <= 128 && p.occ == 1) t_px *= 1.5;                           // the large-W 128-thread tile alone on its SM
+    c.per_harmonic[k] = busiest_cta_steps(p, g) * conc * p.G * p.tw * t_px;
+    c.finish[k] = k > 1 ? 6.0 + px * (8.0 * k + 4.0) / 4.0e6 : 0.0;
+  }
+  c.ok = true;
+  return c;
+}
+
+// the group count for H harmonics in the fused kernel (n = 0 is not one of them)
+int pick_groups(const GroupCosts& c, int H) {
+  if (!c.ok || H < 2) return 1;
   const double margin = FBF_TUNABLE(GROUP_MARGIN, kGroupMargin);
-  auto cost = [&](int k) { return ((H + k - 1) / k) * (rows / (ctas / k) + u); };
   int groups = 1;
-  double best = cost(1);
-  for (int k = 2; k <= std::min({8, H, ctas}); ++k) {
-    const double c = cost(k);
-    if (c < margin * best) best = c, groups = k;
+  double best = H * c.per_harmonic[1];
+  for (int k = 2; k <= std::min(8, H); ++k) {
+    const double t = ((H + k - 1) / k) * c.per_harmonic[k] + c.finish[k];
+    if (t < margin * best) best = t, groups = k;
   }
 #ifdef FBF_EXPERIMENTS
-  if (const char* e = getenv("FBF_GROUPS")) groups = std::max(1, std::min(8, atoi(e)));
+  if (const char* e = getenv("FBF_GROUPS")) groups = std::max(1, std::min({8, H, atoi(e)}));
 #endif
   return groups;
 }
 
-// (Q, P) planes the workspace holds for this geometry: the most any harmonic
-// count (per launch: <= kMaxD) picks (memoised per thread: the host entry asks
-// several times per call)
-int group_cap(const fbf_geometry* g, int radius) {
-  struct Memo {
-    int out_rows = -1, width = -1, batch = -1, radius = -1, dev = -1, cap = 1;
-  };
-  thread_local Memo m;
+// per thread: the costs of the last few geometries (the host pipeline cycles
+// through a handful of chunk shapes) and the most planes any harmonic count
+// picks for them -- the (Q, P) planes the workspace holds
+struct GroupMemo {
+  int out_rows = -1, width = -1, batch = -1, radius = -1, dev = -1;
+  GroupCosts gauss, boxc;
+  int cap = 1;
+};
+const GroupMemo& group_memo(const fbf_geometry* g, int radius) {
+  constexpr int kSlots = 8;
+  thread_local GroupMemo memo[kSlots];
+  thread_local int next = 0;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (m.out_rows == g->out_rows && m.width == g->width && m.batch == g->batch && m.radius == radius && m.dev == dev)
-    return m.cap;
-  int cap = 1;
-  for (int H = 2; H <= kMaxD && cap < 8; ++H) cap = std::max(cap, group_model(g, radius, H));
-  m = Memo{g->out_rows, g->width, g->batch, radius, dev, cap};
-  return cap;
+  for (const GroupMemo& m : memo)
+    if (m.out_rows == g->out_rows && m.width == g->width && m.batch == g->batch && m.radius == radius && m.dev == dev)
+      return m;
+  GroupMemo& m = memo[next];
+  next = (next + 1) % kSlots;
+  m = GroupMemo{};
+  m.out_rows = g->out_rows, m.width = g->width, m.batch = g->batch, m.radius = radius, m.dev = dev;
+  m.gauss = group_costs_of(g, radius, false);
+  m.boxc = group_costs_of(g, radius, true);
+  for (int H = 2; H <= kMaxD && m.cap < 8; ++H)
+    m.cap = std::max({m.cap, pick_groups(m.gauss, H), pick_groups(m.boxc, H)});
+#ifdef FBF_EXPERIMENTS
+  if (getenv("FBF_GROUPS")) m.cap = 8;
+#endif
+  return m;
 }
 
-int harmonic_groups(const fbf_geometry* g, int radius, int harmonics) {
-  return std::min(group_model(g, radius, std::min(harmonics, kMaxD)), group_cap(g, radius));
+int group_cap(const fbf_geometry* g, int radius) { return group_memo(g, radius).cap; }
+
+// groups for a fused run over `harmonics` harmonics n >= 1
+int harmonic_groups(const fbf_geometry* g, int radius, bool box, int harmonics) {
+  const GroupMemo& m = group_memo(g, radius);
+  return std::min(pick_groups(box ? m.boxc : m.gauss, std::min(harmonics, kMaxD)), m.cap);
 }
 
 struct Layout {
@@ -839,14 +978,14 @@ int fbf_filter_prepared_device(const fbf_geometry* gp, const fbf_filter* f, floa
     cudaError_t e = cudaSuccess;
     bool divided = false;
     const int groups =
-        launch_fused_range(A, f, 0, P.H.N + 1, harmonic_groups(gp, f->radius, P.H.N + 1), false, st, &e, &divided);
+        launch_fused_range(A, f, 0, P.H.N + 1, harmonic_groups(gp, f->radius, f->kind == FBF_SPATIAL_BOX, P.H.N), false, st, &e,
+                           &divided);
     FBF_CUDA(e);
     if (!divided) {
       const int cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
       const long long plane = static_cast<long long>(P.G.batch) * P.G.out_rows * cols;
-      finish_groups<<<rows_grid(P.G), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), groups, P.H.N + 1, plane,
-                                                    cols, P.G, P.H.shift, P.H.q_floor, d_bad, dst, nullptr, P.H.aq,
-                                                    P.fmax);
+      launch_finish_groups(st, reinterpret_cast<const p2*>(P.pq), groups, P.H.N + 1, plane, cols, P.G, P.H.shift,
+                           P.H.q_floor, d_bad, dst, nullptr, P.H.aq, P.fmax);
       FBF_CUDA(cudaGetLastError());
     }
     return FBF_OK;
@@ -890,7 +1029,9 @@ int fbf_partial_sums_device(const fbf_geometry* gp, const fbf_filter* f, int n_l
   if (P.variant == FBF_VARIANT_FUSED) {
     const FusedArgs A = fused_args(P, nullptr, nullptr);
     cudaError_t e = cudaSuccess;
-    groups = launch_fused_range(A, f, n_lo, n_hi, harmonic_groups(gp, f->radius, n_hi - n_lo), true, st, &e);
+    groups = launch_fused_range(A, f, n_lo, n_hi,
+                                harmonic_groups(gp, f->radius, f->kind == FBF_SPATIAL_BOX, n_hi - std::max(n_lo, 1)), true,
+                                st, &e);
     FBF_CUDA(e);
     cols = (P.G.width + kFusedTW - 1) / kFusedTW * kFusedTW;
     plane = static_cast<long long>(P.G.batch) * P.G.out_rows * cols;
@@ -898,9 +1039,8 @@ int fbf_partial_sums_device(const fbf_geometry* gp, const fbf_filter* f, int n_l
     if ((rc = naive_range(P, f, n_lo, n_hi, st))) return rc;
     span = 1;
   }
-  finish_groups<<<rows_grid(P.G), 256, 0, st>>>(reinterpret_cast<const p2*>(P.pq), groups, span, plane, cols, P.G,
-                                                0.f, 0.f, nullptr, nullptr, reinterpret_cast<double2*>(pq_out), P.H.aq,
-                                                P.fmax);
+  launch_finish_groups(st, reinterpret_cast<const p2*>(P.pq), groups, span, plane, cols, P.G, 0.f, 0.f, nullptr,
+                       nullptr, reinterpret_cast<double2*>(pq_out), P.H.aq, P.fmax);
   FBF_CUDA(cudaGetLastError());
   return FBF_OK;
 }
@@ -922,7 +1062,7 @@ int fbf_finish_device(const fbf_geometry* gp, const fbf_filter* f, const double*
 
 int fbf_harmonic_groups(const fbf_geometry* g, int radius, int N) {
   if (!g || check_geometry(g) != FBF_OK || N < 0) return 0;
-  return std::min(harmonic_groups(g, radius, N + 1), N + 1);
+  return N < 1 ? 1 : std::min(harmonic_groups(g, radius, false, N), N);  // Gaussian windows (the kind is not part of this query)
 }
 
 int fbf_launches_per_call(const fbf_geometry* g, const fbf_filter* f, int variant) {
@@ -936,7 +1076,7 @@ int fbf_launches_per_call(const fbf_geometry* g, const fbf_filter* f, int varian
     if (f->N == 0) return 3;  // prep, n = 0 plane, divide
     const int chunks = (f->N - 1 + kMaxD) / kMaxD;
     if (chunks > 1) return 2 + chunks;
-    return 3 + (std::min(harmonic_groups(g, f->radius, f->N + 1), f->N) > 1 ? 1 : 0);
+    return 3 + (std::min(harmonic_groups(g, f->radius, f->kind == FBF_SPATIAL_BOX, f->N), f->N) > 1 ? 1 : 0);
   }
   const int tap_uploads = (2 * f->radius + 1 + kTapChunk - 1) / kTapChunk;
   return 1 + tap_uploads + 4 * (f->N + 1) + 1;

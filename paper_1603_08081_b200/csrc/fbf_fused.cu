@@ -5,7 +5,7 @@
 
 namespace fbf {
 
-#define FBF_EXTERN(WW, BB) extern template cudaError_t launch_w<WW, BB>(const FusedArgs&, cudaStream_t, int*);
+#define FBF_EXTERN(WW, BB) extern template cudaError_t launch_w<WW, BB>(const FusedArgs&, cudaStream_t, FusedPlan*);
 #define FBF_RADII(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) \
   X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32) X(33) \
   X(34) X(35) X(36) X(37) X(38) X(39) X(40)
@@ -34,7 +34,7 @@ bool fused_supported(int W, bool box) {
 static unsigned long long* g_prof = nullptr;
 #endif
 
-cudaError_t launch_fused(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
+cudaError_t launch_fused(const FusedArgs& a_in, cudaStream_t st, FusedPlan* plan) {
   FusedArgs a = a_in;
 #ifdef FBF_PHASE_PROF
   if (!g_prof) {
@@ -47,7 +47,7 @@ cudaError_t launch_fused(const FusedArgs& a_in, cudaStream_t st, int* grid_out) 
     switch (a.k.W) {
 #define FBF_CASE_B(WW) \
   case WW:             \
-    return launch_w<WW, true>(a, st, grid_out);
+    return launch_w<WW, true>(a, st, plan);
       FBF_BOX_RADII(FBF_CASE_B)
 #undef FBF_CASE_B
       default: return cudaErrorInvalidValue;
@@ -56,7 +56,7 @@ cudaError_t launch_fused(const FusedArgs& a_in, cudaStream_t st, int* grid_out) 
   switch (a.k.W) {
 #define FBF_CASE(WW) \
   case WW:           \
-    return launch_w<WW>(a, st, grid_out);
+    return launch_w<WW>(a, st, plan);
     FBF_RADII(FBF_CASE)
 #undef FBF_CASE
     default: return cudaErrorInvalidValue;

@@ -64,6 +64,16 @@ struct FusedCfg {
   static constexpr bool QT = QT_;
   static_assert(!QT || (NT == 256 && G == 32 && KC == 16), "TMEM (Q, P): 8 warps, 16 steps of 32 rows");
   static constexpr bool CS64 = QT && W + G <= 64;
+  // CSA: the CS ring is keyed on the OUTPUT row, (row - y0) mod CRING, with
+  // CRING a multiple of 16: a column-pass lane's 16-row window starts on a
+  // multiple of 16 and never wraps, so its 16 centre loads are one base plus
+  // compile-time offsets (the per-load wrap arithmetic was ~3 % of all
+  // executed instructions at c2).  Costs up to 15 more ring rows; the box
+  // kernels keep the W + G ring (their 3 CTAs per SM do not fit the padding).
+#ifndef FBF_CSA
+#define FBF_CSA 1
+#endif
+  static constexpr bool CSA = CS64 || (FBF_CSA != 0 && !BOX_);
   // PQG: the running (Q, P) rows are loaded by their own column-pass lane from
   // global memory (L2; written by the same lane in the previous harmonic:
   // program order, no proxy fence) instead of a per-step TMA tile in shared
@@ -81,7 +91,7 @@ struct FusedCfg {
   static constexpr int MW = TW + 2 * W;   // modulated row width
   static constexpr int MP = MW | 1;       // M plane pitch in 8-byte units (odd: conflict-free row walks)
   static constexpr int RING = 2 * W + G;  // R ring rows
-  static constexpr int CRING = CS64 ? 64 : W + G;  // CS ring rows
+  static constexpr int CRING = CS64 ? 64 : CSA ? (W + G + 15) / 16 * 16 : W + G;  // CS ring rows
   static constexpr int RP = TW + 1;       // R plane pitch in 8-byte units (row-major R)
   // Column-major R (RCOL): plane h, column x, ring slot: (h TW + x) RPT + slot,
   // RPT = RING rounded up to 2 mod 4 (a 2 RPT-word stride = 4 mod 8: the
@@ -440,9 +450,9 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restric
   };
   const int rel = a + g - base;
   const int slot = rel % C::RING;
-  // CS slot of input row rel: CS64 keys it on the output row (rel - W) mod 64,
+  // CS slot of input row rel: CSA keys it on the output row (rel - W) mod CRING,
   // so the column pass's 16-row windows start on multiples of 16 and never wrap
-  const int cslot = C::CS64 ? ((rel + 64 - C::W) & 63) : rel % C::CRING;
+  const int cslot = C::CSA ? (rel + C::CRING - C::W) % C::CRING : rel % C::CRING;
   float* __restrict__ csrow = CS + 2 * cslot * C::CP + h;
   p2 acc[C::KR];
   if constexpr (C::BOX) {
@@ -611,8 +621,8 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
   clk.mark(5);
   // (q, p) = c (Gc, Fc) + s (Gs, Fs)   [bilateral.hpp:138-144, real form]:
   // this lane's half of every row now; the halves meet in Pending::qp
-  if constexpr (C::CS64) {
-    const float* __restrict__ csw = CS + 2 * (((r0 - u.y0) & 63) * C::CP + x) + h;  // window start: a multiple of 16
+  if constexpr (C::CSA) {
+    const float* __restrict__ csw = CS + 2 * (((r0 - u.y0) % C::CRING) * C::CP + x) + h;  // window start: a multiple of 16
 #pragma unroll
     for (int i = 0; i < C::KC; ++i) {
       const float w = csw[2 * i * C::CP];
@@ -934,7 +944,7 @@ inline cudaError_t encode_tile_3d(CUtensorMap* m, const void* base, unsigned lon
 }
 
 template <class C>
-cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
+cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, FusedPlan* plan) {
   constexpr int W = C::W;
   static_assert(C::TW == kFusedTW, "workspace layout assumes kFusedTW-wide strips");
   FusedArgs a = a_in;
@@ -944,15 +954,7 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
   // a unit's prologue row-passes 2W rows without a column pass or demodulation
   // (~55 % of a full row's cost, measured: FBF_UNIT_COST_PCT sweep)
   a.unit_cost = static_cast<int>(2 * W * FBF_TUNABLE(UNIT_COST_FRAC, kUnitCostFrac));
-  cudaError_t e = encode_tile_3d(&a.tm_uf, a.uf, static_cast<unsigned long long>(a.pq_cols + 2 * W),
-                                 static_cast<unsigned long long>(a.g.out_rows + 2 * W),
-                                 static_cast<unsigned long long>(a.g.batch), C::MW, C::G);
-  if (e != cudaSuccess) return e;
   if (a.groups < 1) a.groups = 1;
-  e = encode_tile_3d(&a.tm_pq, a.pq, static_cast<unsigned long long>(a.pq_cols),
-                     static_cast<unsigned long long>(a.g.out_rows),
-                     static_cast<unsigned long long>(a.g.batch) * a.groups, C::TW, C::G);
-  if (e != cudaSuccess) return e;
   // per device, once: the smem opt-in and the resident CTAs per SM (host calls
   // that would otherwise sit on every launch's critical path)
   struct DevInfo {
@@ -960,7 +962,7 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
   };
   thread_local DevInfo info;
   int dev = 0;
-  e = cudaGetDevice(&dev);
+  cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (info.dev != dev) {
     e = cudaFuncSetAttribute(fused_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -981,7 +983,6 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
   const long long by_work = (a.total + min_rows - 1) / min_rows;
   if (grid > by_work) grid = by_work;
   if (grid < 1) grid = 1;
-  if (grid_out) *grid_out = static_cast<int>(grid);
   // L2-resident units: every harmonic re-reads a unit's (u, f') tiles and
   // read-modify-writes its (Q, P) rows.  When the CTAs' long runs (c5: 1,024-row
   // images, 148 CTAs) make that working set exceed L2, it streams from HBM
@@ -1004,6 +1005,19 @@ cudaError_t launch_cfg(const FusedArgs& a_in, cudaStream_t st, int* grid_out) {
 #ifdef FBF_EXPERIMENTS
   a.seg_max = static_cast<int>(FBF_TUNABLE(SEG_MAX, a.seg_max));
 #endif
+  if (plan) {
+    *plan = FusedPlan{static_cast<int>(grid), occ, sms, std::min(a.seg_max, C::SEG), C::G, C::PROLOGUE, C::KC, C::TW,
+                      C::NT, a.unit_cost, C::BOX ? 1 : 0};
+    return cudaSuccess;
+  }
+  e = encode_tile_3d(&a.tm_uf, a.uf, static_cast<unsigned long long>(a.pq_cols + 2 * W),
+                     static_cast<unsigned long long>(a.g.out_rows + 2 * W),
+                     static_cast<unsigned long long>(a.g.batch), C::MW, C::G);
+  if (e != cudaSuccess) return e;
+  e = encode_tile_3d(&a.tm_pq, a.pq, static_cast<unsigned long long>(a.pq_cols),
+                     static_cast<unsigned long long>(a.g.out_rows),
+                     static_cast<unsigned long long>(a.g.batch) * a.groups, C::TW, C::G);
+  if (e != cudaSuccess) return e;
   fused_kernel<C><<<dim3(static_cast<unsigned>(grid), static_cast<unsigned>(a.groups)), C::NT, C::smem_bytes, st>>>(a);
   return cudaGetLastError();
 }
@@ -1220,14 +1234,14 @@ inline bool qt_fits(const FusedArgs& a, int groups, int seg_rows) {
 }
 
 template <int W, bool BOX = false>
-cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
+cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, FusedPlan* plan) {
   if (a.n0_only) return launch_n0<W, BOX>(a, st);
   using Small = FusedCfg<W, 64, 16, 16, 16, 128, BOX>;
   using Big = FusedCfg<W, 64, 32, 16, 16, 256, BOX>;
 #ifdef FBF_EXPERIMENTS  // TMEM (Q, P): measured slower (profiles/r02_notes.md), experiment build only
   using BigQ = FusedCfg<W, 64, 32, 16, 16, 256, BOX, true>;
   if constexpr (!BOX && W > 9 && BigQ::FITS) {
-    if (FBF_TUNABLE(QT, 0) != 0 && qt_fits(a, std::max(1, a.groups), BigQ::SEG)) return launch_cfg<BigQ>(a, st, grid_out);
+    if (FBF_TUNABLE(QT, 0) != 0 && qt_fits(a, std::max(1, a.groups), BigQ::SEG)) return launch_cfg<BigQ>(a, st, plan);
   }
 #endif
 #ifdef FBF_EXPERIMENTS
@@ -1237,12 +1251,12 @@ cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
 #endif
   if constexpr (Small::smem_bytes <= 113 * 1024) {  // two 128-thread CTAs per SM
     const bool big = env ? env[0] == 'b' : !(W <= 9);
-    if (!big || !Big::FITS) return launch_cfg<Small>(a, st, grid_out);
+    if (!big || !Big::FITS) return launch_cfg<Small>(a, st, plan);
   }
   if constexpr (Big::FITS) {
-    return launch_cfg<Big>(a, st, grid_out);
+    return launch_cfg<Big>(a, st, plan);
   } else if constexpr (Small::FITS) {  // large W: one 128-thread CTA per SM
-    return launch_cfg<Small>(a, st, grid_out);
+    return launch_cfg<Small>(a, st, plan);
   } else {
     (void)env;
     return cudaErrorInvalidValue;
@@ -1252,6 +1266,6 @@ cudaError_t launch_w(const FusedArgs& a, cudaStream_t st, int* grid_out) {
 }  // namespace fbf
 
 #define FBF_INSTANTIATE_FUSED(WW) \
-  template cudaError_t fbf::launch_w<WW, false>(const fbf::FusedArgs&, cudaStream_t, int*);
+  template cudaError_t fbf::launch_w<WW, false>(const fbf::FusedArgs&, cudaStream_t, fbf::FusedPlan*);
 #define FBF_INSTANTIATE_FUSED_BOX(WW) \
-  template cudaError_t fbf::launch_w<WW, true>(const fbf::FusedArgs&, cudaStream_t, int*);
+  template cudaError_t fbf::launch_w<WW, true>(const fbf::FusedArgs&, cudaStream_t, fbf::FusedPlan*);

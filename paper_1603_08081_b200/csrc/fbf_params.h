@@ -94,4 +94,17 @@ struct FusedArgs {
   Harmonics h;     // last: the coefficient block is the large member
 };
 
+// What a launch of this geometry looks like (the harmonic-group cost model in
+// fbf_capi.cu simulates the kernel's own CTA cuts from it): launch_fused with
+// a FusedPlan pointer fills it and launches nothing.
+struct FusedPlan {
+  int grid;       // CTAs per harmonic group (grid.x)
+  int occ;        // resident CTAs per SM of this instance
+  int sms;
+  int seg_max;    // unit cap in rows
+  int G, prologue, kc, tw, nt;
+  int unit_cost;  // rows (the kernel's cut coordinate)
+  int box;
+};
+
 }  // namespace fbf

@@ -21,10 +21,11 @@ inline double tunable(const char* env, double dflt) {
 #define FBF_TUNABLE(name, dflt) (dflt)
 #endif
 
-// harmonic-group cost model (fbf_capi.cu group_model): the unit prologue in
-// rows of one harmonic per 2W, and the margin a larger group count must win by
+// the fused kernel's cut coordinate: a unit's prologue in rows of one harmonic
+// per 2W (fbf_fused.cuh); the margin a larger harmonic-group count must win by
+// in the group cost model (fbf_capi.cu pick_groups; the finish pass is in the model)
 constexpr double kUnitCostFrac = 0.55;
-constexpr double kGroupMargin = 0.97;
+constexpr double kGroupMargin = 0.99;
 // host pipeline (fbf_hostpath.cpp plan_chunks)
 constexpr double kPipelineMinPx = 1.0e6;  // calls below this many pixels run as one launch
 constexpr int kBatchChunks = 16;          // image chunks of a batch call
