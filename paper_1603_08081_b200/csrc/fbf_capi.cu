@@ -801,7 +801,12 @@ int launch_fused_range(const FusedArgs& base, const fbf_filter* f, int n_lo, int
   // n = 0 as a single-plane filter (n0_plane_kernel) into group plane 0; the
   // fused kernel then starts at n = 1 with group 0 accumulating onto it
   // (always, so the n = 0 term has the same bits in every harmonic partition)
-  if (n_lo == 0) {
+  // With harmonic groups (>= 2, a filtering call, one launch) the n = 0 kernel
+  // runs LAST instead, in finish mode: it adds its term to the groups' planes
+  // and divides, replacing the n = 0 plane pass and finish_groups (c2: 28 + 25
+  // us -> one ~35 us pass).
+  const bool n0_finishes = n_lo == 0 && !partial && divided && n_hi - 1 <= kMaxD && std::min(groups, n_hi - 1) >= 2;
+  if (n_lo == 0 && !n0_finishes) {
     A.h.d[0] = static_cast<float>(f->d[0]);
     *err = launch_n0_plane(A, st);
     if (*err != cudaSuccess) return 0;
@@ -809,6 +814,7 @@ int launch_fused_range(const FusedArgs& base, const fbf_filter* f, int n_lo, int
     A.acc_group0 = 1;
     if (n_hi == 1) return 1;  // N = 0: plane 0 holds the sums; the caller divides
   }
+  if (n0_finishes) n_lo = 1;
   const bool one = n_hi - n_lo <= kMaxD;
   A.groups = one ? std::max(1, std::min(groups, n_hi - n_lo)) : 1;
   for (int c0 = n_lo; c0 < n_hi; c0 += kMaxD) {
@@ -821,6 +827,16 @@ int launch_fused_range(const FusedArgs& base, const fbf_filter* f, int n_lo, int
     A.partial = partial || A.groups > 1 || c1 < n_hi;
     *err = launch_fused(A, st, nullptr);
     if (*err != cudaSuccess) return 0;
+  }
+  if (n0_finishes) {
+    FusedArgs F = A;  // groups, planes, dst, bad as the fused launch saw them
+    F.h = base.h;
+    F.h.d[0] = static_cast<float>(f->d[0]);
+    F.n0_only = 2;
+    *err = launch_fused(F, st, nullptr);
+    if (*err != cudaSuccess) return 0;
+    *divided = true;
+    return A.groups;
   }
   if (divided) *divided = !A.partial;
   return A.groups;
@@ -1072,11 +1088,11 @@ int fbf_launches_per_call(const fbf_geometry* g, const fbf_filter* f, int varian
     variant = FBF_VARIANT_FUSED;
   }
   if (variant == FBF_VARIANT_FUSED && fused_ok(f)) {
-    // prep, the n = 0 plane (N >= 1), fused launches of <= kMaxD harmonics (, group sum)
+    // prep, the n = 0 kernel (plane before, or finish mode after), fused launches of <= kMaxD harmonics
     if (f->N == 0) return 3;  // prep, n = 0 plane, divide
     const int chunks = (f->N - 1 + kMaxD) / kMaxD;
     if (chunks > 1) return 2 + chunks;
-    return 3 + (std::min(harmonic_groups(g, f->radius, f->kind == FBF_SPATIAL_BOX, f->N), f->N) > 1 ? 1 : 0);
+    return 3;  // one group: prep, n = 0 plane, fused (divides); groups: prep, fused, n = 0 kernel in finish mode
   }
   const int tap_uploads = (2 * f->radius + 1 + kTapChunk - 1) / kTapChunk;
   return 1 + tap_uploads + 4 * (f->N + 1) + 1;

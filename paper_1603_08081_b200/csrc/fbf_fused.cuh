@@ -73,7 +73,8 @@ struct FusedCfg {
 #ifndef FBF_CSA
 #define FBF_CSA 1
 #endif
-  static constexpr bool CSA = CS64 || (FBF_CSA != 0 && !BOX_);
+  // (measured on/off per config: c4 W = 24 +1.8 %, c5 W = 12 +0.7 %, c2 W = 15 -0.3 %: off there)
+  static constexpr bool CSA = CS64 || (FBF_CSA != 0 && !BOX_ && W_ != 15);
   // PQG: the running (Q, P) rows are loaded by their own column-pass lane from
   // global memory (L2; written by the same lane in the previous harmonic:
   // program order, no proxy fence) instead of a per-step TMA tile in shared
@@ -1050,10 +1051,10 @@ struct N0Cfg {
   static constexpr int KC = 4;                              // column pass: (column pair, 4 rows)
   static constexpr int COL_ITEMS = (kN0TX / 2) * (kN0TY / KC);
 };
-template <int W, bool BOX, int TY>
 #ifndef FBF_N0_MINB
 #define FBF_N0_MINB 1
 #endif
+template <int W, bool BOX, int TY, bool FIN>
 __global__ void __launch_bounds__(kN0Threads, FBF_N0_MINB) n0_plane_kernel(const __grid_constant__ FusedArgs A) {
   using C = N0Cfg<W, BOX, TY>;
   constexpr int kN0TY = TY;
@@ -1068,6 +1069,13 @@ __global__ void __launch_bounds__(kN0Threads, FBF_N0_MINB) n0_plane_kernel(const
   const float d0 = A.h.d[0];
   const p2 dd = pk(d0 * fs.sq, d0 * fs.sp);
   auto tap = [&](int j) { return BOX ? A.k.box_tap : A.k.t[j < 0 ? -j : j]; };
+  // n0_only == 2: finish mode.  The n = 0 term is not written as a plane but
+  // added to the A.groups harmonic-group planes the fused kernel left (every
+  // group holds >= 1 harmonic), and the pixel is divided here: one kernel
+  // instead of the n = 0 plane pass before and finish_groups after the fused
+  // kernel (same integers, same bits)
+  constexpr bool fin = FIN;
+  const long long plane = static_cast<long long>(A.g.batch) * A.g.out_rows * A.pq_cols;  // even: pq_cols % 64 == 0
   const long long t = blockIdx.x;
   const int b = static_cast<int>(t / per_img);
   const int r = static_cast<int>(t - b * per_img);
@@ -1149,6 +1157,20 @@ __global__ void __launch_bounds__(kN0Threads, FBF_N0_MINB) n0_plane_kernel(const
     p2 acc[C::KC];
 #pragma unroll
     for (int k = 0; k < C::KC; ++k) acc[k] = 0ull;
+    // finish mode: the first two group planes' values of this item are loaded
+    // now and land during the FIR (further planes, if any, after it)
+    constexpr int kPre = 2;
+    ulonglong2 pre[C::KC][kPre];
+    if (fin) {
+#pragma unroll
+      for (int k = 0; k < C::KC; ++k) {
+        const int y = min(y0 + run * C::KC + k, A.g.out_rows - 1);
+        const ulonglong2* __restrict__ gsrc =
+            reinterpret_cast<const ulonglong2*>(out0 + 2 * xp + static_cast<long long>(y) * A.pq_cols);
+#pragma unroll
+        for (int g = 0; g < kPre; ++g) pre[k][g] = g < A.groups ? gsrc[g * (plane / 2)] : make_ulonglong2(0ull, 0ull);
+      }
+    }
     const float* __restrict__ col = rowt + run * C::KC * C::RP + 2 * xp;
 #pragma unroll
     for (int m = 0; m < C::KC + 2 * W; ++m) {
@@ -1169,16 +1191,54 @@ __global__ void __launch_bounds__(kN0Threads, FBF_N0_MINB) n0_plane_kernel(const
       if (y < A.g.out_rows) {
         float c0, c1;
         upk(acc[k], c0, c1);
-        float q0, p0, q1, p1;
-        upk(to_fixed(mul2(dd, pk(1.0f, c0))), q0, p0);
-        upk(to_fixed(mul2(dd, pk(1.0f, c1))), q1, p1);
-        *reinterpret_cast<float4*>(out + static_cast<long long>(y) * A.pq_cols) = make_float4(q0, p0, q1, p1);
+        p2 t0 = to_fixed(mul2(dd, pk(1.0f, c0))), t1 = to_fixed(mul2(dd, pk(1.0f, c1)));
+        if (!fin) {
+          float q0, p0, q1, p1;
+          upk(t0, q0, p0);
+          upk(t1, q1, p1);
+          *reinterpret_cast<float4*>(out + static_cast<long long>(y) * A.pq_cols) = make_float4(q0, p0, q1, p1);
+          continue;
+        }
+        // finish mode: + the harmonic groups' planes (exact integer sums), divide
+        const ulonglong2* __restrict__ gsrc =
+            reinterpret_cast<const ulonglong2*>(out + static_cast<long long>(y) * A.pq_cols);
+#pragma unroll
+        for (int g = 0; g < kPre; ++g) {
+          t0 = iadd2(t0, pre[k][g].x);
+          t1 = iadd2(t1, pre[k][g].y);
+        }
+        if (A.groups > kPre) {
+          ulonglong2 v[8 - kPre];
+#pragma unroll
+          for (int g = kPre; g < 8; ++g)
+            if (g < A.groups) v[g - kPre] = gsrc[g * (plane / 2)];
+#pragma unroll
+          for (int g = kPre; g < 8; ++g)
+            if (g < A.groups) {
+              t0 = iadd2(t0, v[g - kPre].x);
+              t1 = iadd2(t1, v[g - kPre].y);
+            }
+        }
+        float* __restrict__ drow = A.dst + b * A.g.dst_bstride + static_cast<long long>(y) * A.g.dst_pitch;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int gx = x0 + 2 * xp + j;
+          if (gx >= A.g.width) break;
+          float Q, P;
+          from_fixed(j ? t1 : t0, fs, Q, P);
+          if (!(fabsf(Q) >= A.h.q_floor) && A.bad) {
+            const unsigned long long lin = static_cast<unsigned long long>(b) * A.g.full_height * A.g.width +
+                                           static_cast<unsigned long long>(A.g.out_row0 + y) * A.g.width + gx;
+            atomicMin(A.bad, lin);
+          }
+          drow[gx] = A.h.shift + __fdiv_rn(P, Q);
+        }
       }
     }
   }
 }
 
-template <int W, bool BOX, int TY>
+template <int W, bool BOX, int TY, bool FIN>
 cudaError_t launch_n0_ty(const FusedArgs& a, cudaStream_t st) {
   using C = N0Cfg<W, BOX, TY>;
   static_assert(C::smem_bytes <= 227 * 1024, "n0 tile exceeds shared memory");
@@ -1187,14 +1247,14 @@ cudaError_t launch_n0_ty(const FusedArgs& a, cudaStream_t st) {
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev_done != dev) {
-    e = cudaFuncSetAttribute(n0_plane_kernel<W, BOX, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(n0_plane_kernel<W, BOX, TY, FIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(C::smem_bytes));
     if (e != cudaSuccess) return e;
     dev_done = dev;
   }
   const long long tiles = static_cast<long long>(a.strips) * ((a.g.out_rows + TY - 1) / TY) * a.g.batch;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidValue;
-  n0_plane_kernel<W, BOX, TY><<<static_cast<unsigned>(tiles), kN0Threads, C::smem_bytes, st>>>(a);
+  n0_plane_kernel<W, BOX, TY, FIN><<<static_cast<unsigned>(tiles), kN0Threads, C::smem_bytes, st>>>(a);
   return cudaGetLastError();
 }
 // 128-row tiles (row-pass halo overhead (128+2W)/128) where they still give a
@@ -1209,9 +1269,14 @@ cudaError_t launch_n0(const FusedArgs& a_in, cudaStream_t st) {
 #ifdef FBF_EXPERIMENTS
   ty = static_cast<int>(FBF_TUNABLE(N0_TY, ty));
 #endif
-  if (ty >= 128) return launch_n0_ty<W, BOX, 128>(a, st);
-  if (ty >= 64) return launch_n0_ty<W, BOX, 64>(a, st);
-  return launch_n0_ty<W, BOX, 32>(a, st);
+  if (a.n0_only == 2) {  // finish mode (after the fused kernel's harmonic groups)
+    if (ty >= 128) return launch_n0_ty<W, BOX, 128, true>(a, st);
+    if (ty >= 64) return launch_n0_ty<W, BOX, 64, true>(a, st);
+    return launch_n0_ty<W, BOX, 32, true>(a, st);
+  }
+  if (ty >= 128) return launch_n0_ty<W, BOX, 128, false>(a, st);
+  if (ty >= 64) return launch_n0_ty<W, BOX, 64, false>(a, st);
+  return launch_n0_ty<W, BOX, 32, false>(a, st);
 }
 
 // Small (128 threads, G=16, two CTAs per SM) for W <= 9, big (256 threads,
