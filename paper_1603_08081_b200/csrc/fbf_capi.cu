@@ -571,8 +571,10 @@ void fill_harmonics(Harmonics& h, const fbf_filter* f) {
 // plan mode); a unit's prologue steps count 0.8 of a full step (c2: one group
 // 995 us, two groups 946 us, i.e. 15.6 against 29.6 / 2 steps per harmonic).
 // Step time: per pixel and harmonic on one SM, linear in the taps (fitted to
-// c5 / c2 / c4 at W = 12 / 15 / 24).  The finish pass moves 8 k + 4 bytes per
-// pixel at ~4 TB/s plus ~6 us.  Measured: profiles/r02_notes.md (groups).
+// c5 / c2 / c4 at W = 12 / 15 / 24).  With groups the n = 0 kernel runs last, in
+// finish mode, and reads the k planes (8 k bytes per pixel at ~4 TB/s; c2,
+// k = 2: 42 us against 28 us for the plain n = 0 plane pass).  Measured:
+// profiles/r02_notes.md (groups).
 constexpr double kModelPrologueStep = 0.8;
 struct GroupCosts {
   double per_harmonic[9] = {};  // [k]: busiest CTA's time for one harmonic, us
@@ -633,7 +635,7 @@ GroupCosts group_costs_of(const fbf_geometry* g, int radius, bool box) {
                       : (0.86 + 0.0757 * (2.0 * radius + 1.0)) / 2048.0;  // us per pixel and harmonic on one SM
     if (p.nt <= 128 && p.occ == 1) t_px *= 1.5;                           // the large-W 128-thread tile alone on its SM
     c.per_harmonic[k] = busiest_cta_steps(p, g) * conc * p.G * p.tw * t_px;
-    c.finish[k] = k > 1 ? 6.0 + px * (8.0 * k + 4.0) / 4.0e6 : 0.0;
+    c.finish[k] = k > 1 ? 2.0 + px * 8.0 * k / 4.0e6 : 0.0;  // the n = 0 kernel in finish mode reads k planes more
   }
   c.ok = true;
   return c;

@@ -60,6 +60,7 @@ struct HostCtx {
   int dev = -1;
   cudaStream_t st[2] = {nullptr, nullptr};  // chunk streams (copies of one chunk overlap the kernels of the other)
   cudaEvent_t ev[2] = {nullptr, nullptr};   // per stream: the last strip's H2D (halo rows of the next strip)
+  cudaEvent_t kdone[2] = {nullptr, nullptr};  // per stream: the last chunk's kernels finished (kernel order = chunk order)
   cudaEvent_t done[kMaxChunks] = {};        // per chunk: its D2H landed (f64 output conversion)
   cudaEvent_t join = nullptr;               // stream 1 back into stream 0
   unsigned long long* h_bad = nullptr;      // pinned: per-chunk collapse indices (graph-capturable read-back)
@@ -74,6 +75,7 @@ struct HostCtx {
     dev = d;
     for (auto& s : st) FBF_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     for (auto& e : ev) FBF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : kdone) FBF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : done) FBF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     FBF_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
     FBF_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_bad), kMaxChunks * sizeof(unsigned long long)));
@@ -109,6 +111,8 @@ struct HostCtx {
     for (auto s : st)
       if (s) cudaStreamDestroy(s);
     for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto e : kdone)
       if (e) cudaEventDestroy(e);
     for (auto e : done)
       if (e) cudaEventDestroy(e);
@@ -422,11 +426,20 @@ struct Pipeline {
       if (e == cudaSuccess) e = cudaEventRecord(ctx->ev[k & 1], st);
       if (e != cudaSuccess) return cuda_fail(e, "event");
     }
+    // Kernels run in chunk order: chunk k's start behind chunk k-1's last
+    // kernel.  Every fused kernel fills the GPU, so nothing is lost; without
+    // the edge, chunk k's fused kernel can take the SMs ahead of chunk k-1's
+    // closing n = 0 / finish kernel (ready at the same moment on the other
+    // stream) and hold back that chunk's D2H, and the H2D queued behind it, for
+    // a whole kernel (c2 e2e 1.34 -> 1.54 ms when that happened).
+    if (K > 1 && k > 0 && (e = cudaStreamWaitEvent(st, ctx->kdone[(k - 1) & 1], 0)) != cudaSuccess)
+      return cuda_fail(e, "event");
     const fbf_geometry gc = chunk_geometry(c);
     const int rc = fbf_bilateral_fast_device(&gc, f, d_src + c.b0 * sb + static_cast<long long>(c.s0 - g->src_row0) * g->width,
                                              d_dst + c.b0 * db + static_cast<long long>(c.o0 - g->out_row0) * g->width,
                                              ws0 + (k & 1) * (nws > 1 ? ws_bytes : 0), ws_bytes, d_bad + k, v, st);
     if (rc != FBF_OK) return rc;
+    if (K > 1 && (e = cudaEventRecord(ctx->kdone[k & 1], st)) != cudaSuccess) return cuda_fail(e, "event");
     const bool dst_stacked = c.o0 == g->out_row0 && c.o1 == g->out_row0 + g->out_rows &&
                              dst_bstride == static_cast<long long>(g->out_rows) * dst_pitch;
     for (int b = c.b0; b < c.b0 + c.nb; b += dst_stacked ? c.nb : 1) {
