@@ -577,8 +577,8 @@ void fill_harmonics(Harmonics& h, const fbf_filter* f) {
 // profiles/r02_notes.md (groups).
 constexpr double kModelPrologueStep = 0.8;
 struct GroupCosts {
-  double per_harmonic[9] = {};  // [k]: busiest CTA's time for one harmonic, us
-  double finish[9] = {};        // [k]: finish_groups, us
+  double per_harmonic[kMaxGroups + 1] = {};  // [k]: busiest CTA's time for one harmonic, us
+  double finish[kMaxGroups + 1] = {};        // [k]: the finish pass, us
   bool ok = false;
 };
 
@@ -626,7 +626,7 @@ GroupCosts group_costs_of(const fbf_geometry* g, int radius, bool box) {
   A.k.box = box;
   A.seg_max = 1 << 30;
   const double px = static_cast<double>(g->batch) * g->out_rows * g->width;
-  for (int k = 1; k <= 8; ++k) {
+  for (int k = 1; k <= kMaxGroups; ++k) {
     A.groups = k;
     FusedPlan p{};
     if (launch_fused(A, nullptr, &p) != cudaSuccess || p.grid < 1) return c;  // no device: one group
@@ -647,12 +647,12 @@ int pick_groups(const GroupCosts& c, int H) {
   const double margin = FBF_TUNABLE(GROUP_MARGIN, kGroupMargin);
   int groups = 1;
   double best = H * c.per_harmonic[1];
-  for (int k = 2; k <= std::min(8, H); ++k) {
+  for (int k = 2; k <= std::min(kMaxGroups, H); ++k) {
     const double t = ((H + k - 1) / k) * c.per_harmonic[k] + c.finish[k];
     if (t < margin * best) best = t, groups = k;
   }
 #ifdef FBF_EXPERIMENTS
-  if (const char* e = getenv("FBF_GROUPS")) groups = std::max(1, std::min({8, H, atoi(e)}));
+  if (const char* e = getenv("FBF_GROUPS")) groups = std::max(1, std::min({kMaxGroups, H, atoi(e)}));
 #endif
   return groups;
 }
@@ -680,10 +680,10 @@ const GroupMemo& group_memo(const fbf_geometry* g, int radius) {
   m.out_rows = g->out_rows, m.width = g->width, m.batch = g->batch, m.radius = radius, m.dev = dev;
   m.gauss = group_costs_of(g, radius, false);
   m.boxc = group_costs_of(g, radius, true);
-  for (int H = 2; H <= kMaxD && m.cap < 8; ++H)
+  for (int H = 2; H <= kMaxD && m.cap < kMaxGroups; ++H)
     m.cap = std::max({m.cap, pick_groups(m.gauss, H), pick_groups(m.boxc, H)});
 #ifdef FBF_EXPERIMENTS
-  if (getenv("FBF_GROUPS")) m.cap = 8;
+  if (getenv("FBF_GROUPS")) m.cap = kMaxGroups;
 #endif
   return m;
 }

@@ -1207,17 +1207,16 @@ __global__ void __launch_bounds__(kN0Threads, FBF_N0_MINB) n0_plane_kernel(const
           t0 = iadd2(t0, pre[k][g].x);
           t1 = iadd2(t1, pre[k][g].y);
         }
-        if (A.groups > kPre) {
-          ulonglong2 v[8 - kPre];
+        for (int g0 = kPre; g0 < A.groups; g0 += 4) {  // further planes, four loads in flight
+          ulonglong2 v[4];
 #pragma unroll
-          for (int g = kPre; g < 8; ++g)
-            if (g < A.groups) v[g - kPre] = gsrc[g * (plane / 2)];
+          for (int i = 0; i < 4; ++i)
+            v[i] = g0 + i < A.groups ? gsrc[(g0 + i) * (plane / 2)] : make_ulonglong2(0ull, 0ull);
 #pragma unroll
-          for (int g = kPre; g < 8; ++g)
-            if (g < A.groups) {
-              t0 = iadd2(t0, v[g - kPre].x);
-              t1 = iadd2(t1, v[g - kPre].y);
-            }
+          for (int i = 0; i < 4; ++i) {
+            t0 = iadd2(t0, v[i].x);
+            t1 = iadd2(t1, v[i].y);
+          }
         }
         float* __restrict__ drow = A.dst + b * A.g.dst_bstride + static_cast<long long>(y) * A.g.dst_pitch;
 #pragma unroll

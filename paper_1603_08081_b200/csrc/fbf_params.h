@@ -8,6 +8,7 @@
 namespace fbf {
 
 constexpr int kMaxD = 256;     // harmonic coefficients carried by one fused launch
+constexpr int kMaxGroups = 16; // harmonic groups (CTA groups with their own (Q, P) plane) of one fused launch
 constexpr int kMaxN = 65535;   // highest harmonic accepted (larger N: several fused launches)
 constexpr int kFusedTW = 64;  // column-strip width of the fused kernel (workspace layout)
 constexpr int kMaxWFused = 64;      // taps carried in the fused kernel's parameter block (W <= this)
