@@ -114,15 +114,35 @@ __global__ void prep_padded_kernel(const float* __restrict__ src, int2* __restri
   const int pw = cols + 2 * W, ph = g.out_rows + 2 * W;
   const long long nrows = static_cast<long long>(ph) * g.batch;
   float m = 0.f;
-  for (long long r = blockIdx.y; r < nrows; r += gridDim.y) {
-    const int b = static_cast<int>(r / ph), py = static_cast<int>(r - static_cast<long long>(b) * ph);
-    const int gy = mirror_index(g.out_row0 - W + py, g.full_height) - g.src_row0;
-    const float* __restrict__ srow = src + b * g.src_bstride + static_cast<long long>(gy) * g.src_pitch;
-    int4* __restrict__ urow = reinterpret_cast<int4*>(uf + r * pw);
+  // kPrepRows padded rows per thread and pass, every load issued before the
+  // first use (a pure streaming kernel: with one row in flight per thread it
+  // ran at ~2 TB/s, c2 24.8 us)
+  constexpr int kPrepRows = 4;
+  for (long long r0 = blockIdx.y; r0 < nrows; r0 += static_cast<long long>(kPrepRows) * gridDim.y) {
+    const float* srow[kPrepRows];
+#pragma unroll
+    for (int j = 0; j < kPrepRows; ++j) {
+      const long long r = min(r0 + static_cast<long long>(j) * gridDim.y, nrows - 1);
+      const int b = static_cast<int>(r / ph), py = static_cast<int>(r - static_cast<long long>(b) * ph);
+      const int gy = mirror_index(g.out_row0 - W + py, g.full_height) - g.src_row0;
+      srow[j] = src + b * g.src_bstride + static_cast<long long>(gy) * g.src_pitch;
+    }
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; 2 * q < pw; q += gridDim.x * blockDim.x) {
-      const int2 a = phase_of(srow[mirror_index(2 * q - W, g.width)], turns_scaled, shift, m);
-      const int2 c = phase_of(srow[mirror_index(2 * q + 1 - W, g.width)], turns_scaled, shift, m);
-      urow[q] = make_int4(a.x, a.y, c.x, c.y);
+      const int x0 = mirror_index(2 * q - W, g.width), x1 = mirror_index(2 * q + 1 - W, g.width);
+      float f0[kPrepRows], f1[kPrepRows];
+#pragma unroll
+      for (int j = 0; j < kPrepRows; ++j) {
+        f0[j] = __ldg(srow[j] + x0);
+        f1[j] = __ldg(srow[j] + x1);
+      }
+#pragma unroll
+      for (int j = 0; j < kPrepRows; ++j) {
+        const long long r = r0 + static_cast<long long>(j) * gridDim.y;
+        if (r >= nrows) break;
+        const int2 a = phase_of(f0[j], turns_scaled, shift, m);
+        const int2 c = phase_of(f1[j], turns_scaled, shift, m);
+        reinterpret_cast<int4*>(uf + r * pw)[q] = make_int4(a.x, a.y, c.x, c.y);
+      }
     }
   }
   note_fmax(m, fmax);

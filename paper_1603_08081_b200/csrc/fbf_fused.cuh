@@ -457,24 +457,30 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restric
   float* __restrict__ csrow = CS + 2 * cslot * C::CP + h;
   p2 acc[C::KR];
   if constexpr (C::BOX) {
-    // running sum over the window [i, i+2W] (unweighted)
+    // running sum over the window [i, i+2W] (unweighted).  Every input is
+    // loaded before the first add or centre store: with two adds per load
+    // there is nothing to hide a load -> store / load -> add latency behind
+    // (ncu, c3: the centre stores and the adds sat on short-scoreboard stalls
+    // for 28 % of the kernel's samples when each load was used at once)
+    p2 in[TAPS_IN];
+#pragma unroll
+    for (int m = 0; m < TAPS_IN; ++m) in[m] = src[m];
     p2 sum = 0ull;
 #pragma unroll
     for (int m = 0; m <= 2 * C::W; ++m) {
-      const p2 v = src[m];
-      sum = add2(sum, v);
-      if (m >= C::W && m < C::W + C::KR && live) csrow[2 * (xc + m - C::W)] = lo_of(v);
+      sum = add2(sum, in[m]);
       defer_at(m);
     }
     acc[0] = sum;
 #pragma unroll
     for (int i = 1; i < C::KR; ++i) {
-      const p2 vin = src[i + 2 * C::W], vout = src[i - 1];
-      sum = sub2(add2(sum, vin), vout);
+      sum = sub2(add2(sum, in[i + 2 * C::W]), in[i - 1]);
       acc[i] = sum;
-      const int m = i + 2 * C::W;
-      if (m >= C::W && m < C::W + C::KR && live) csrow[2 * (xc + m - C::W)] = lo_of(vin);
       defer_at(2 * C::W + i);
+    }
+    if (live) {
+#pragma unroll
+      for (int i = 0; i < C::KR; ++i) csrow[2 * (xc + i)] = lo_of(in[i + C::W]);
     }
   } else {
 #pragma unroll
@@ -568,16 +574,20 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
     v1 = t.y;
   };
   if constexpr (C::BOX) {
+    // all ring rows of the lane's window first (see the row pass)
+    p2 in[TAPS_IN];
+#pragma unroll
+    for (int m = 0; m < TAPS_IN; ++m) in[m] = ring(m);
     p2 sum = 0ull;
 #pragma unroll
     for (int m = 0; m <= 2 * C::W; ++m) {
-      sum = add2(sum, ring(m));
+      sum = add2(sum, in[m]);
       batch(m);
     }
     acc[0] = sum;
 #pragma unroll
     for (int i = 1; i < C::KC; ++i) {
-      sum = sub2(add2(sum, ring(i + 2 * C::W)), ring(i - 1));
+      sum = sub2(add2(sum, in[i + 2 * C::W]), in[i - 1]);
       acc[i] = sum;
       batch(i + 2 * C::W);
     }
@@ -1084,22 +1094,26 @@ __global__ void __launch_bounds__(kN0Threads, FBF_N0_MINB) n0_plane_kernel(const
   const int2* __restrict__ img = A.uf + static_cast<long long>(b) * ph * pw;
   float* in1 = reinterpret_cast<float*>(in2);
   static_assert(C::IW % 2 == 0 && C::RP % 2 == 0, "pairs");
-  // load: warp = padded rows, lane = 16-byte column pairs (4 rows in flight)
+  // load: warp = padded rows, lane = 16-byte column pairs; LR rows in flight
+  // per warp (the plane-mode kernel has registers to spare: shared memory
+  // limits it to 2-3 CTAs per SM, and its load phase was latency-bound:
+  // long-scoreboard stalls 27 % of the samples)
   {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int NP = C::IW / 2;  // IW even
     constexpr int PER = (NP + 31) / 32;
-    for (int y4 = warp * 4; y4 < C::IH; y4 += 4 * (kN0Threads / 32)) {
-      int4 v[4][PER];
+    constexpr int LR = FIN ? 4 : 8;
+    for (int y4 = warp * LR; y4 < C::IH; y4 += LR * (kN0Threads / 32)) {
+      int4 v[LR][PER];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
+      for (int r = 0; r < LR; ++r) {
         const int py = min(y0 + min(y4 + r, C::IH - 1), ph - 1);  // past the image: clamped, never stored
         const int4* __restrict__ row = reinterpret_cast<const int4*>(img + static_cast<long long>(py) * pw + x0);
 #pragma unroll
         for (int c = 0; c < PER; ++c) v[r][c] = __ldg(row + min(lane + 32 * c, NP - 1));
       }
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
+      for (int r = 0; r < LR; ++r) {
         const int yy = y4 + r;
         if (yy < C::IH) {
           float* dst = in1 + 2 * ((yy >> 1) * C::IWP) + (yy & 1);
