@@ -122,3 +122,37 @@ def test_host_entry_is_reentrant_across_threads():
     for t in range(2):
         for k in range(4):
             assert np.array_equal(got[t][k], want[(k + t) % 4])
+
+
+def test_group_model_picks_and_finish_mode():
+    """The harmonic-group model (the kernel's own cuts replayed on the launch plan): c2 splits its
+    harmonics in two (step granularity + prologues), the long runs of c4 / c5 stay in one group, the small
+    c1 takes one harmonic per group; the count never exceeds the planes the workspace holds (16).  With
+    groups the n = 0 kernel closes the call in finish mode: three launches (prep, fused, n = 0), and the
+    result equals the partial-sums route (fused + finish_groups) bit for bit."""
+    import torch
+    picks = {}
+    for name, c in CONFIGS.items():
+        g = fb.whole_geometry(c.width, c.height, c.batch)
+        picks[name] = fb.harmonic_groups(g, spatial_of(c).radius, c.N)
+        assert 1 <= picks[name] <= 16
+        assert fb.launches_per_call(g, spatial_of(c), approx_of(c)) == 3
+    assert picks["c2"] == 2 and picks["c4"] == 1 and picks["c5"] == 1 and picks["c1"] >= 6, picks
+    # finish mode (filter) against partial sums over the full range + fbf_finish_device
+    c = CONFIGS["c1"]
+    img, s, a = image_of(c), spatial_of(c), approx_of(c)
+    geo = fb.whole_geometry(c.width, c.height)
+    out = run_device(img, geo, s, a)[0]
+    dev = torch.device("cuda", 0)
+    src = torch.from_numpy(np.ascontiguousarray(img, dtype=np.float32)).to(dev)
+    ws = torch.empty(fb.workspace_bytes(geo, s.radius, "fused"), dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    fb.prepare_device(src.data_ptr(), geo, s, a, ws.data_ptr(), ws.numel(), st)
+    pq = torch.empty((c.height, c.width, 2), dtype=torch.float64, device=dev)
+    fb.partial_sums_device(pq.data_ptr(), geo, s, a, 0, a.N + 1, ws.data_ptr(), ws.numel(), st)
+    dst = torch.empty((c.height, c.width), dtype=torch.float32, device=dev)
+    bad = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    fb.finish_device(pq.data_ptr(), dst.data_ptr(), geo, s, a, bad.data_ptr(), st)
+    torch.cuda.synchronize()
+    assert int(bad.item()) == -1
+    assert np.array_equal(dst.cpu().numpy(), out)
