@@ -654,7 +654,6 @@ GroupCosts group_costs_of(const fbf_geometry* g, int radius, bool box) {
     double t_px = box ? 0.70e-3 * (kFusedTW + 2.0 * radius) / 74.0
                       : (0.86 + 0.0757 * (2.0 * radius + 1.0)) / 2048.0;  // us per pixel and harmonic on one SM
     if (p.nt <= 128 && p.occ == 1) t_px *= 1.5;                           // the large-W 128-thread tile alone on its SM
-    if (p.box == 2) t_px = 0.45e-3;                                       // the small-box kernel (fbf_box2.cuh)
     c.per_harmonic[k] = busiest_cta_steps(p, g) * conc * p.G * p.tw * t_px;
     c.finish[k] = k > 1 ? 2.0 + px * 8.0 * k / 4.0e6 : 0.0;  // the n = 0 kernel in finish mode reads k planes more
   }

@@ -34,14 +34,8 @@ bool fused_supported(int W, bool box) {
 static unsigned long long* g_prof = nullptr;
 #endif
 
-// small box windows: the register-column kernel (fbf_box2.cuh); FBF_BOX2=0 in
-// the experiment build falls back to the general kernel's box instances
-bool box2_supported(int W);
-cudaError_t launch_box2_any(const FusedArgs& a, cudaStream_t st, FusedPlan* plan);
-
 cudaError_t launch_fused(const FusedArgs& a_in, cudaStream_t st, FusedPlan* plan) {
   FusedArgs a = a_in;
-  if (a.k.box && !a.n0_only && box2_supported(a.k.W) && FBF_TUNABLE(BOX2, 1) != 0) return launch_box2_any(a, st, plan);
 #ifdef FBF_PHASE_PROF
   if (!g_prof) {
     cudaMalloc(&g_prof, (32 + 4 * 1024) * sizeof(unsigned long long));
