@@ -1199,6 +1199,27 @@ __global__ void __launch_bounds__(kN0Threads, FBF_N0_MINB) n0_plane_kernel(const
       }
     }
     Pair* __restrict__ out = out0 + 2 * xp;
+    if (fin) {  // further planes (many groups: small images), two at a time for all KC rows: 8 loads in flight
+      for (int g0 = kPre; g0 < A.groups; g0 += 2) {
+        ulonglong2 v[C::KC][2];
+#pragma unroll
+        for (int k = 0; k < C::KC; ++k) {
+          const int y = min(y0 + run * C::KC + k, A.g.out_rows - 1);
+          const ulonglong2* __restrict__ gsrc =
+              reinterpret_cast<const ulonglong2*>(out + static_cast<long long>(y) * A.pq_cols);
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+            v[k][i] = g0 + i < A.groups ? gsrc[(g0 + i) * (plane / 2)] : make_ulonglong2(0ull, 0ull);
+        }
+#pragma unroll
+        for (int k = 0; k < C::KC; ++k)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            pre[k][0].x = iadd2(pre[k][0].x, v[k][i].x);
+            pre[k][0].y = iadd2(pre[k][0].y, v[k][i].y);
+          }
+      }
+    }
 #pragma unroll
     for (int k = 0; k < C::KC; ++k) {
       const int y = y0 + run * C::KC + k;
@@ -1214,23 +1235,10 @@ __global__ void __launch_bounds__(kN0Threads, FBF_N0_MINB) n0_plane_kernel(const
           continue;
         }
         // finish mode: + the harmonic groups' planes (exact integer sums), divide
-        const ulonglong2* __restrict__ gsrc =
-            reinterpret_cast<const ulonglong2*>(out + static_cast<long long>(y) * A.pq_cols);
 #pragma unroll
         for (int g = 0; g < kPre; ++g) {
           t0 = iadd2(t0, pre[k][g].x);
           t1 = iadd2(t1, pre[k][g].y);
-        }
-        for (int g0 = kPre; g0 < A.groups; g0 += 4) {  // further planes, four loads in flight
-          ulonglong2 v[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            v[i] = g0 + i < A.groups ? gsrc[(g0 + i) * (plane / 2)] : make_ulonglong2(0ull, 0ull);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            t0 = iadd2(t0, v[i].x);
-            t1 = iadd2(t1, v[i].y);
-          }
         }
         float* __restrict__ drow = A.dst + b * A.g.dst_bstride + static_cast<long long>(y) * A.g.dst_pitch;
 #pragma unroll
