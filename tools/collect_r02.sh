@@ -8,6 +8,7 @@ cp $A/bench_default.json $P/r02_bench_default.json
 cp $A/bench_reference.json $P/r02_bench_reference.json
 cp $A/bench_c2_naive.json $P/r02_bench_c2_naive.json
 cp $A/launches_c2.csv $P/r02_launches_c2.csv
+for c in c1 c3 c5; do [ -f $A/launches_$c.csv ] && cp $A/launches_$c.csv $P/r02_launches_$c.csv; done
 cp $A/pytest_gpu.log $P/r02_pytest_gpu.log
 cp $A/shake.log $P/r02_shake.txt
 cp $A/gpu.txt $P/r02_gpu.txt

@@ -18,6 +18,9 @@ CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > $A/plain_launch.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $A/launches_c2.csv $CMD > $A/ncu_launch.log 2>&1
 echo "ncu launches rc=$?"
+for c in c1 c3 c5; do
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $A/launches_$c.csv python bench.py --config $c --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+done
 for c in c2 c1 c3 c4 c5; do
   python bench.py --profile-once --config $c > $A/plain_$c.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:fused_kernel -c 1 -f -o $A/prof_fused_$c python bench.py --profile-once --config $c > $A/ncu_full_$c.log 2>&1
