@@ -550,10 +550,19 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
   const int s0 = (r0 - C::W - base) % C::RING;
   constexpr int TAPS_IN = C::KC + 2 * C::W;
   constexpr int NBATCH = ModNext<C>::NBATCH;
-#ifndef FBF_MOD_OFF
-#define FBF_MOD_OFF 12
+  // Where the next step's modulation starts inside the column FIR (visit
+  // index q).  The outside-in order visits the window's edge rows first, which
+  // feed only one or two outputs each (q-th input: ~q/2 + 1 FFMA2): the loop is
+  // FMA-dense, with issue slots to spare for the modulation's ALU work, only
+  // from q ~ 2 KC on.  Start there, leaving 4 visits per batch before the end.
+  // Measured against the old fixed 12: c5 (W = 12) 6,055 -> 6,245 Mpixel/s, c4
+  // (W = 24) 2,009 -> 2,069, c2 (W = 15) 4,120 -> 4,159 (profiles/r02_notes.md).
+#ifdef FBF_MOD_OFF
+  constexpr int MOD_OFF = FBF_MOD_OFF;
+#else
+  constexpr int MOD_OFF = TAPS_IN - 4 * NBATCH < 2 * C::KC ? (TAPS_IN - 4 * NBATCH > 0 ? TAPS_IN - 4 * NBATCH : 0) : 2 * C::KC;
 #endif
-  constexpr int OFF = (C::BOX || TAPS_IN <= FBF_MOD_OFF + NBATCH) ? 0 : FBF_MOD_OFF;
+  constexpr int OFF = (C::BOX || TAPS_IN <= MOD_OFF + NBATCH) ? 0 : MOD_OFF;
   constexpr int STRIDE = (TAPS_IN - OFF) / NBATCH > 0 ? (TAPS_IN - OFF) / NBATCH : 1;
   // one batch of (up to) 4 modulation elements of the next step per STRIDE taps
   auto batch = [&](int m) {
@@ -1227,32 +1236,32 @@ __global__ void __launch_bounds__(kN0Threads, FBF_N0_MINB) n0_plane_kernel(const
         float c0, c1;
         upk(acc[k], c0, c1);
         p2 t0 = to_fixed(mul2(dd, pk(1.0f, c0))), t1 = to_fixed(mul2(dd, pk(1.0f, c1)));
-        if (!fin) {
+        if constexpr (!FIN) {
           float q0, p0, q1, p1;
           upk(t0, q0, p0);
           upk(t1, q1, p1);
           *reinterpret_cast<float4*>(out + static_cast<long long>(y) * A.pq_cols) = make_float4(q0, p0, q1, p1);
-          continue;
-        }
-        // finish mode: + the harmonic groups' planes (exact integer sums), divide
+        } else {
+          // finish mode: + the harmonic groups' planes (exact integer sums), divide
 #pragma unroll
-        for (int g = 0; g < kPre; ++g) {
-          t0 = iadd2(t0, pre[k][g].x);
-          t1 = iadd2(t1, pre[k][g].y);
-        }
-        float* __restrict__ drow = A.dst + b * A.g.dst_bstride + static_cast<long long>(y) * A.g.dst_pitch;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int gx = x0 + 2 * xp + j;
-          if (gx >= A.g.width) break;
-          float Q, P;
-          from_fixed(j ? t1 : t0, fs, Q, P);
-          if (!(fabsf(Q) >= A.h.q_floor) && A.bad) {
-            const unsigned long long lin = static_cast<unsigned long long>(b) * A.g.full_height * A.g.width +
-                                           static_cast<unsigned long long>(A.g.out_row0 + y) * A.g.width + gx;
-            atomicMin(A.bad, lin);
+          for (int g = 0; g < kPre; ++g) {
+            t0 = iadd2(t0, pre[k][g].x);
+            t1 = iadd2(t1, pre[k][g].y);
           }
-          drow[gx] = A.h.shift + __fdiv_rn(P, Q);
+          float* __restrict__ drow = A.dst + b * A.g.dst_bstride + static_cast<long long>(y) * A.g.dst_pitch;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int gx = x0 + 2 * xp + j;
+            if (gx >= A.g.width) break;
+            float Q, P;
+            from_fixed(j ? t1 : t0, fs, Q, P);
+            if (!(fabsf(Q) >= A.h.q_floor) && A.bad) {
+              const unsigned long long lin = static_cast<unsigned long long>(b) * A.g.full_height * A.g.width +
+                                             static_cast<unsigned long long>(A.g.out_row0 + y) * A.g.width + gx;
+              atomicMin(A.bad, lin);
+            }
+            drow[gx] = A.h.shift + __fdiv_rn(P, Q);
+          }
         }
       }
     }
