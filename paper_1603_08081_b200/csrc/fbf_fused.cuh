@@ -554,13 +554,15 @@ __device__ __forceinline__ void col_pass(const FusedArgs& A, const p2* __restric
   // index q).  The outside-in order visits the window's edge rows first, which
   // feed only one or two outputs each (q-th input: ~q/2 + 1 FFMA2): the loop is
   // FMA-dense, with issue slots to spare for the modulation's ALU work, only
-  // from q ~ 2 KC on.  Start there, leaving 4 visits per batch before the end.
-  // Measured against the old fixed 12: c5 (W = 12) 6,055 -> 6,245 Mpixel/s, c4
-  // (W = 24) 2,009 -> 2,069, c2 (W = 15) 4,120 -> 4,159 (profiles/r02_notes.md).
+  // from q ~ 2 KC on.  Start there, leaving >= 4 visits per batch before the end
+  // (W = 12: 24, W >= 14: 32).  Measured against the old fixed 12: c5 (W = 12)
+  // 6,055 -> 6,230 Mpixel/s, c4 (W = 24) 2,009 -> 2,069, c2 (W = 15) 4,120 ->
+  // 4,177; sweeps in profiles/r02_notes.md.
 #ifdef FBF_MOD_OFF
   constexpr int MOD_OFF = FBF_MOD_OFF;
 #else
-  constexpr int MOD_OFF = TAPS_IN - 4 * NBATCH < 2 * C::KC ? (TAPS_IN - 4 * NBATCH > 0 ? TAPS_IN - 4 * NBATCH : 0) : 2 * C::KC;
+  constexpr int MOD_ROOM = TAPS_IN - 4 * NBATCH > 0 ? (TAPS_IN - 4 * NBATCH) / 8 * 8 : 0;  // a multiple of 8 visits
+  constexpr int MOD_OFF = MOD_ROOM < 2 * C::KC ? MOD_ROOM : 2 * C::KC;
 #endif
   constexpr int OFF = (C::BOX || TAPS_IN <= MOD_OFF + NBATCH) ? 0 : MOD_OFF;
   constexpr int STRIDE = (TAPS_IN - OFF) / NBATCH > 0 ? (TAPS_IN - OFF) / NBATCH : 1;
