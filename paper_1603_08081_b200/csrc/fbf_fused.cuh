@@ -359,6 +359,11 @@ struct PhaseClock {
 #define FBF_DEFER_Q0 8
 #endif
 constexpr int kDeferQ0 = FBF_DEFER_Q0;  // first row-pass input position of the deferred finishes
+// The finishes end where the ascending row FIR stops being FMA-dense (its last
+// KR inputs feed fewer and fewer outputs), but stay >= 3 inputs apart:
+// BACK = min(KR, inputs - Q0 - 3 KH) inputs before the end.  Measured per radius
+// (BACK 0 / 8 / 14 at W = 12: 6,243 / 6,259 / 6,234; at W = 15: 4,158 / 4,160 /
+// 4,208; BACK 0 / 12 / 20 at W = 24: 2,066 / 2,074 / 2,052 Mpixel/s).
 
 template <class C>
 struct Pending {
@@ -444,10 +449,16 @@ __device__ __forceinline__ void row_pass(const FusedArgs& A, const p2* __restric
   if (!C::DEFER && !live) return;
   const p2* __restrict__ src = M + (h * C::G + g) * C::MP + xc;
   constexpr int TAPS_IN = C::KR + 2 * C::W;
+#ifdef FBF_DEFER_BACK
+  constexpr int BACK = FBF_DEFER_BACK;
+#else
+  constexpr int ROOM = TAPS_IN - kDeferQ0 - 3 * (C::KC / 2);
+  constexpr int BACK = ROOM < 0 ? 0 : ROOM < C::KR ? ROOM : C::KR;
+#endif
   auto defer_at = [&](int m) {  // finish pending row k at input position m (compile-time)
 #pragma unroll
     for (int k = 0; k < Pending<C>::KH; ++k)
-      if (C::DEFER && m == kDeferQ0 + k * (TAPS_IN - kDeferQ0) / Pending<C>::KH) pd.finish(k, h, A.pq_cols);
+      if (C::DEFER && m == kDeferQ0 + k * (TAPS_IN - BACK - kDeferQ0) / Pending<C>::KH) pd.finish(k, h, A.pq_cols);
   };
   const int rel = a + g - base;
   const int slot = rel % C::RING;
