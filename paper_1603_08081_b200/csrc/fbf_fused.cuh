@@ -73,8 +73,9 @@ struct FusedCfg {
 #ifndef FBF_CSA
 #define FBF_CSA 1
 #endif
-  // (measured on/off per config: c4 W = 24 +1.8 %, c5 W = 12 +0.7 %, c2 W = 15 -0.3 %: off there)
-  static constexpr bool CSA = CS64 || (FBF_CSA != 0 && !BOX_ && W_ != 15);
+  // (measured on / off per config: c4 W = 24 +1.8 %, c5 W = 12 +0.7 %, c2 W = 15 -0.3 % when it was
+  // introduced, +0.1-0.3 % after the modulation / finish placement changes: on for every radius)
+  static constexpr bool CSA = CS64 || (FBF_CSA != 0 && !BOX_);
   // PQG: the running (Q, P) rows are loaded by their own column-pass lane from
   // global memory (L2; written by the same lane in the previous harmonic:
   // program order, no proxy fence) instead of a per-step TMA tile in shared
